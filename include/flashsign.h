@@ -1,0 +1,100 @@
+/*
+ * flashsign.h -- C-ABI of the B200-native FlashSign (spherical attention) forward.
+ *
+ * This is the drop-in boundary for the reference hot path.  The reference
+ * (arxiv 2505.09326, package `ncstream`, pure Python) has no FFI of its own;
+ * each entry point below replaces one reference interface:
+ *
+ *   fs_fwd          <- ncstream.attention.streamed_attention_array
+ *                      (pkg/src/ncstream/attention.py:252-279) and its batched
+ *                      caller multi_head_attention_array (attention.py:318-361):
+ *                      one launch covers every (batch, head, query tile); query
+ *                      head h reads kv head (h*heads_kv)/heads_q (attention.py:352).
+ *                      Errors mirror ShapeMismatchError (tensor.py:32-33,
+ *                      attention.py:104-111, 339-344), ConfigError
+ *                      (attention.py:36-37, 54-56, 77-80, 337-338) and
+ *                      DegenerateDenominatorError (normalizers.py:29-35,
+ *                      attention.py:196-199) -- the latter reported on the device
+ *                      through `bad_key` (below) because the launch is async.
+ *   fs_query_tile   <- the transient score tile recorded by ScoreBufferMeter
+ *                      (attention.py:86-97, 169-171).
+ *   fs_last_error   <- the exception message text.
+ *
+ * Math (normalizers.py:94-100, SPHERICAL; eps = denom_epsilon, normalizers.py:69):
+ *     s_ij = scale * q_descale * k_descale * (q_i . k_j)
+ *     O_i  = v_descale * sum_j s_ij v_j / sqrt(sum_j s_ij^2 + eps)
+ *
+ * No torch types cross this boundary: plain device pointers, element strides,
+ * sizes and a cudaStream_t.  All calls are asynchronous on `stream`.
+ */
+#ifndef FLASHSIGN_H
+#define FLASHSIGN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *fs_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  FS_OK = 0,
+  FS_ERR_SHAPE = 1,       /* -> ShapeMismatchError  */
+  FS_ERR_CONFIG = 2,      /* -> ConfigError         */
+  FS_ERR_DTYPE = 3,       /* -> ShapeMismatchError (dtype) */
+  FS_ERR_UNSUPPORTED = 4, /* -> ConfigError (outside the kernel envelope) */
+  FS_ERR_CUDA = 5         /* -> RuntimeError        */
+} fs_status;
+
+typedef enum {
+  FS_F16 = 0,
+  FS_BF16 = 1,
+  FS_E4M3 = 2,
+  FS_F32 = 3 /* output only */
+} fs_dtype;
+
+/* Sentinel value of *bad_key when no row was degenerate. */
+#define FS_BAD_NONE 0xFFFFFFFFFFFFFFFFull
+
+typedef struct {
+  /* Device pointers (caller-owned).  Layout BSHD: element (b, n, h, d) lives at
+     ptr[b*stride[0] + n*stride[1] + h*stride[2] + d]; the d stride is 1. */
+  const void *q, *k, *v;
+  void *o;
+  int64_t q_stride[3], k_stride[3], v_stride[3], o_stride[3];
+  int32_t batch, heads_q, heads_kv, seqlen_q, seqlen_kv, head_dim;
+  fs_dtype in_dtype;  /* FS_F16 | FS_BF16 | FS_E4M3 (q, k, v share it)        */
+  fs_dtype out_dtype; /* FS_F16 | FS_BF16 | FS_F32                              */
+  float scale;        /* score_scale c: finite, may be negative (0: all rows degenerate unless eps>0) */
+  float eps;          /* denom_epsilon >= 0                                    */
+  float p_scale;      /* P = p_scale * s before the PV MMA (FP8: fit e4m3); 1.0 */
+  float q_descale, k_descale, v_descale; /* per-tensor dequant (FP8); 1.0      */
+  /* Optional device scalar (may be NULL).  fs_fwd resets it to FS_BAD_NONE on
+     `stream`, then the kernel atomically keeps the minimum of
+       (linear_row << 32) | float_bits(z),  linear_row = (b*heads_q + h)*seqlen_q + n
+     over rows whose denominator sqrt(z + eps) is 0 or non-finite, i.e. the
+     first bad row in the reference's loop order (batch, head, row) and its z
+     = sum_j s_ij^2.  An FP16/FP8 P overflow is reported as z = +inf. */
+  uint64_t *bad_key;
+  int32_t tile_m_hint, tile_n_hint; /* TileConfig (g_y, s_x); advisory only    */
+} fs_fwd_params;
+
+/* Validate, encode TMA descriptors (cached per call), launch.  Async. */
+fs_status fs_fwd(const fs_fwd_params *p, fs_stream_t stream);
+
+/* Thread-local text of the last non-FS_OK status. */
+const char *fs_last_error(void);
+
+/* Score tile (query rows x keys) held on chip per Q tile for (head_dim, dtype):
+   what ScoreBufferMeter records.  Returns 0 on success. */
+int fs_query_tile(int head_dim, fs_dtype dt, int *bm, int *bn);
+
+/* Library version (major*10000 + minor*100 + patch). */
+int fs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLASHSIGN_H */

@@ -1,0 +1,95 @@
+"""ctypes binding of the FlashSign C-ABI (``include/flashsign.h``).
+
+The shared library ``_lib/libflashsign.so`` is built in-tree by
+``paper_2505_09326_b200/build.py`` (nvcc, sm_100a).  There is no fallback:
+if the library is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libflashsign.so")
+
+FS_OK, FS_ERR_SHAPE, FS_ERR_CONFIG, FS_ERR_DTYPE, FS_ERR_UNSUPPORTED, FS_ERR_CUDA = range(6)
+FS_F16, FS_BF16, FS_E4M3, FS_F32 = range(4)
+FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
+
+# every symbol include/flashsign.h declares
+EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version")
+
+
+class FsFwdParams(ctypes.Structure):
+    """Mirror of ``fs_fwd_params`` (include/flashsign.h)."""
+
+    _fields_ = [
+        ("q", ctypes.c_void_p),
+        ("k", ctypes.c_void_p),
+        ("v", ctypes.c_void_p),
+        ("o", ctypes.c_void_p),
+        ("q_stride", ctypes.c_int64 * 3),
+        ("k_stride", ctypes.c_int64 * 3),
+        ("v_stride", ctypes.c_int64 * 3),
+        ("o_stride", ctypes.c_int64 * 3),
+        ("batch", ctypes.c_int32),
+        ("heads_q", ctypes.c_int32),
+        ("heads_kv", ctypes.c_int32),
+        ("seqlen_q", ctypes.c_int32),
+        ("seqlen_kv", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("in_dtype", ctypes.c_int32),
+        ("out_dtype", ctypes.c_int32),
+        ("scale", ctypes.c_float),
+        ("eps", ctypes.c_float),
+        ("p_scale", ctypes.c_float),
+        ("q_descale", ctypes.c_float),
+        ("k_descale", ctypes.c_float),
+        ("v_descale", ctypes.c_float),
+        ("bad_key", ctypes.c_void_p),
+        ("tile_m_hint", ctypes.c_int32),
+        ("tile_n_hint", ctypes.c_int32),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and return the FlashSign library; raise loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"FlashSign CUDA library not built: {LIB_PATH} is missing. "
+                    "Run `python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)."
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            lib.fs_fwd.argtypes = [ctypes.POINTER(FsFwdParams), ctypes.c_void_p]
+            lib.fs_fwd.restype = ctypes.c_int
+            lib.fs_last_error.argtypes = []
+            lib.fs_last_error.restype = ctypes.c_char_p
+            lib.fs_query_tile.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                          ctypes.POINTER(ctypes.c_int)]
+            lib.fs_query_tile.restype = ctypes.c_int
+            lib.fs_version.argtypes = []
+            lib.fs_version.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    return load().fs_last_error().decode("utf-8", "replace")
+
+
+def query_tile(head_dim: int, dtype_code: int) -> tuple[int, int]:
+    bm, bn = ctypes.c_int(0), ctypes.c_int(0)
+    if load().fs_query_tile(head_dim, dtype_code, ctypes.byref(bm), ctypes.byref(bn)) != 0:
+        raise ValueError(f"no FlashSign tile for head_dim={head_dim} dtype={dtype_code}")
+    return bm.value, bn.value

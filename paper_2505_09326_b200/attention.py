@@ -1,0 +1,344 @@
+"""Drop-in replacement for the reference hot-path API ``ncstream.attention``.
+
+Same names, positional order, defaults and exception types as
+``/root/reference/pkg/src/ncstream/attention.py``:
+
+    streamed_attention_array(q, k, v, spec, scale, tile, f16=False, meter=None)   # :252-279
+    streamed_attention(q, k, v, cfg, meter=None)                                  # :301-315
+    multi_head_attention_array(q, k, v, spec, h, h_kv, scale=None, tile=None,
+                               path="streamed", f16=False, meter=None)            # :318-361
+    multi_head_attention(q, k, v, cfg, h, h_kv, path="streamed", meter=None)      # :364-378
+    naive_attention_array / naive_generalized_attention                           # :114-143, 282-298
+
+The streamed path runs the sm_100a FlashSign kernel (``flashsign.fwd``) on the
+current CUDA device: numpy arrays are copied to the GPU, quantised to the
+compute dtype, computed in one launch (all heads), and the fp32 result is
+copied back in the input's dtype.  There is no CPU fallback: without a CUDA
+device or the built library these functions raise.
+
+Numerics differ from the float64 reference by the compute dtype (tensor cores):
+``f16=True`` computes on binary16 inputs, exactly the values the reference's
+f16 emulation quantises to (attention.py:265-270); otherwise the compute dtype
+is ``get_compute_dtype()`` (default fp16, env ``FLASHSIGN_COMPUTE_DTYPE``).
+S, sum s^2 and O accumulate in fp32; P is rounded to the compute dtype for the
+PV MMA.  The reference's float64 1e-12 tolerances are not attainable on tensor
+cores; tests state the per-dtype tolerances.
+
+The naive path (``path="naive"``, ``naive_attention_array``) materialises the
+full score matrix on the GPU in float64 with torch -- the reference's
+materialising algorithm, also used as the PyTorch-eager context baseline.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, flashsign
+from ._errors import ConfigError
+from .normalizers import DegenerateDenominatorError, NormalizerSpec
+from .tensor import DenseTensor, ShapeMismatchError, quantize_f16_array
+
+__all__ = [
+    "ConfigError", "TileConfig", "AttentionConfig", "ScoreBufferMeter", "default_score_scale",
+    "naive_attention_array", "streamed_attention_array", "naive_generalized_attention",
+    "streamed_attention", "multi_head_attention_array", "multi_head_attention",
+    "apply_multiplicity_array", "apply_multiplicity", "set_compute_dtype", "get_compute_dtype",
+]
+
+_COMPUTE_DTYPES = {"fp16": torch.float16, "bf16": torch.bfloat16}
+if hasattr(torch, "float8_e4m3fn"):
+    _COMPUTE_DTYPES["e4m3"] = torch.float8_e4m3fn
+_compute = os.environ.get("FLASHSIGN_COMPUTE_DTYPE", "fp16")
+
+
+def set_compute_dtype(name: str) -> None:
+    """Select the tensor-core input dtype for float32/float64 arrays: fp16 | bf16 | e4m3."""
+    global _compute
+    if name not in _COMPUTE_DTYPES:
+        raise ConfigError(f"compute dtype must be one of {sorted(_COMPUTE_DTYPES)}, got {name!r}")
+    _compute = name
+
+
+def get_compute_dtype() -> str:
+    return _compute
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """Query-group g_y and stream-chunk s_x (attention.py:40-56).
+
+    On the GPU the tile is a hint: the kernel's tile is fixed per head dim
+    (``fs_query_tile``: 128 x 128).  Validation is identical to the reference.
+    """
+
+    g_y: int = 64
+    s_x: int = 64
+    w: int | None = None
+    t: int | None = None
+
+    def __post_init__(self):
+        if self.g_y < 1 or self.s_x < 1:
+            raise ConfigError(f"tile sizes must be >= 1, got g_y={self.g_y}, s_x={self.s_x}")
+
+
+def default_score_scale(spec: NormalizerSpec, k: int) -> float:
+    """1 for sign-preserving triples, else 1/sqrt(k) (attention.py:59-67)."""
+    if "sign_preserving" in spec.properties:
+        return 1.0
+    return 1.0 / math.sqrt(k)
+
+
+@dataclass(frozen=True)
+class AttentionConfig:
+    """spec + score_scale + tile + f16 flag (attention.py:70-83)."""
+
+    spec: NormalizerSpec
+    score_scale: float | None = None
+    tile: TileConfig = field(default_factory=TileConfig)
+    f16_emulation: bool = False
+
+    def __post_init__(self):
+        if self.score_scale is not None:
+            if not math.isfinite(self.score_scale) or self.score_scale == 0.0:
+                raise ConfigError(f"score_scale must be finite and nonzero, got {self.score_scale}")
+
+    def resolve_scale(self, k: int) -> float:
+        return self.score_scale if self.score_scale is not None else default_score_scale(self.spec, k)
+
+
+class ScoreBufferMeter:
+    """Peak transient score elements (attention.py:86-97).  The streamed GPU
+    path records the kernel's real on-chip tile, min(BM, y) * min(BN, x)."""
+
+    def __init__(self):
+        self.peak_elements = 0
+
+    def record(self, n: int) -> None:
+        if n > self.peak_elements:
+            self.peak_elements = n
+
+    def peak_bytes(self, dtype_bytes: int) -> int:
+        return self.peak_elements * dtype_bytes
+
+
+def _check_qkv(q, k, v):
+    # attention.py:104-111
+    if q.ndim != 2 or k.ndim != 2 or v.ndim != 2:
+        raise ShapeMismatchError(f"expected rank-2 Q/K/V, got {q.shape}, {k.shape}, {v.shape}")
+    if q.shape[1] != k.shape[1]:
+        raise ShapeMismatchError(f"Q and K feature dims differ: {q.shape} vs {k.shape}")
+    if v.shape[0] != k.shape[0]:
+        raise ShapeMismatchError(f"K and V row counts differ: {k.shape} vs {v.shape}")
+    return q.shape[0], k.shape[0], q.shape[1]
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("FlashSign needs a CUDA device (sm_100a); there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _require_spherical(spec) -> None:
+    if getattr(spec, "name", None) != "spherical":
+        raise ConfigError(f"flashsign: only the spherical normaliser runs on the GPU streamed path, "
+                          f"got {getattr(spec, 'name', spec)!r}")
+
+
+def _out_dtype(a: np.ndarray):
+    return a.dtype if a.dtype in (np.float16, np.float32, np.float64) else np.dtype(np.float64)
+
+
+def _to_device(a: np.ndarray, dev, dtype: torch.dtype, d_pad: int) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.dtype not in (torch.float16, torch.float32, torch.float64):
+        t = t.to(torch.float64)
+    t = t.to(dev, non_blocking=False)
+    if t.shape[-1] != d_pad:
+        t = torch.nn.functional.pad(t, (0, d_pad - t.shape[-1]))
+    if dtype == getattr(torch, "float8_e4m3fn", None):
+        t = t.float().clamp_(-448.0, 448.0)
+    return t.to(dtype).contiguous()
+
+
+def _gpu_streamed(q3: np.ndarray, k3: np.ndarray, v3: np.ndarray, scale: float, eps: float,
+                  compute: str, meter) -> np.ndarray:
+    """FlashSign on [n, h, d] / [x, h_kv, d] arrays in one launch; raises the
+    reference's DegenerateDenominatorError for the first bad (head, row)."""
+    n, h, d = q3.shape
+    x, h_kv, _ = k3.shape
+    if v3.shape[2] != d:
+        raise ShapeMismatchError(f"value dim must equal the head dim: {v3.shape} vs {q3.shape}")
+    tdt = _COMPUTE_DTYPES[compute]
+    out_np_dtype = _out_dtype(q3)
+    if meter is not None:
+        bm, bn = _lib.query_tile(min(max(d, 1), 128), _lib.FS_E4M3 if compute == "e4m3" else _lib.FS_BF16)
+        meter.record(min(bm, n) * min(bn, x))
+    if n == 0:
+        return np.empty((0, h, d), dtype=out_np_dtype)
+    if d > 128:
+        raise ConfigError(f"flashsign: head dim {d} > 128 is not supported by the sm_100a kernel")
+    align = 16 if compute == "e4m3" else 8
+    d_pad = max(align, -(-d // align) * align)
+    dev = _device()
+    qt = _to_device(q3, dev, tdt, d_pad)[None]
+    kt = _to_device(k3, dev, tdt, d_pad)[None]
+    vt = _to_device(v3, dev, tdt, d_pad)[None]
+    if x == 0:  # keep TMA descriptors valid for an empty K/V stream
+        kt = torch.zeros((1, 1, h_kv, d_pad), dtype=tdt, device=dev)[:, :0]
+        vt = kt
+    o, bad = flashsign.fwd_async(qt, kt, vt, scale=float(scale), eps=float(eps), out_dtype=torch.float32)
+    info = flashsign.decode_bad_key(int(bad.item()), h, n)
+    if info is not None:
+        _, _, row, z = info
+        raise DegenerateDenominatorError(float(z), f"row {row}")
+    return o[0, :, :, :d].cpu().numpy().astype(out_np_dtype, copy=False)
+
+
+def streamed_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: NormalizerSpec, scale: float,
+                             tile: TileConfig, f16: bool = False, meter: ScoreBufferMeter | None = None) -> np.ndarray:
+    """Streamed path on plain arrays (attention.py:252-279), on the FlashSign kernel."""
+    _check_qkv(q, k, v)
+    _require_spherical(spec)
+    if tile.g_y < 1 or tile.s_x < 1:
+        raise ConfigError(f"tile sizes must be >= 1, got g_y={tile.g_y}, s_x={tile.s_x}")
+    compute = _compute
+    if f16:
+        if q.dtype != np.float32:
+            raise ConfigError("f16 emulation requires float32 inputs")
+        compute = "fp16"
+    out = _gpu_streamed(q[:, None, :], k[:, None, :], v[:, None, :], scale, spec.denom_epsilon, compute, meter)
+    return out[:, 0, :]
+
+
+def multi_head_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: NormalizerSpec, h: int, h_kv: int,
+                               scale: float | None = None, tile: TileConfig | None = None, path: str = "streamed",
+                               f16: bool = False, meter: ScoreBufferMeter | None = None) -> np.ndarray:
+    """Grouped-query multi-head attention on [n, heads, d] (attention.py:318-361).
+
+    All heads run in ONE FlashSign launch; query head i reads kv head
+    (i*h_kv)//h; the first degenerate (head, row) in the reference's loop order
+    is reported.
+    """
+    if h < 1 or h_kv < 1 or h % h_kv != 0:
+        raise ConfigError(f"query heads must be a multiple of kv heads, got h={h}, h_kv={h_kv}")
+    if q.ndim != 3 or k.ndim != 3 or v.ndim != 3:
+        raise ShapeMismatchError(f"expected rank-3 inputs, got {q.shape}, {k.shape}, {v.shape}")
+    if q.shape[1] != h or k.shape[1] != h_kv or v.shape[1] != h_kv:
+        raise ShapeMismatchError(f"head axes do not match h={h}, h_kv={h_kv}: {q.shape}, {k.shape}, {v.shape}")
+    if path not in ("streamed", "naive"):
+        raise ConfigError(f"unknown attention path {path!r}")
+    d = q.shape[2]
+    eff_scale = scale if scale is not None else default_score_scale(spec, d)
+    eff_tile = tile if tile is not None else TileConfig()
+    if path == "naive":
+        out = np.empty(q.shape, dtype=_out_dtype(q))
+        for i in range(h):
+            kv = (i * h_kv) // h
+            out[:, i, :] = naive_attention_array(q[:, i, :], k[:, kv, :], v[:, kv, :], spec, eff_scale, meter)
+        return out
+    if q.shape[2] != k.shape[2]:
+        raise ShapeMismatchError(f"Q and K feature dims differ: {q.shape} vs {k.shape}")
+    if k.shape[0] != v.shape[0]:
+        raise ShapeMismatchError(f"K and V row counts differ: {k.shape} vs {v.shape}")
+    _require_spherical(spec)
+    if eff_tile.g_y < 1 or eff_tile.s_x < 1:
+        raise ConfigError("tile sizes must be >= 1")
+    compute = _compute
+    if f16:
+        if q.dtype != np.float32:
+            raise ConfigError("f16 emulation requires float32 inputs")
+        compute = "fp16"
+    return _gpu_streamed(q, k, v, eff_scale, spec.denom_epsilon, compute, meter)
+
+
+def naive_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: NormalizerSpec, scale: float,
+                          meter: ScoreBufferMeter | None = None) -> np.ndarray:
+    """Materialising path (attention.py:114-143) on the GPU in float64 (torch).
+
+    float32 inputs follow the reference's rounding points: scores rounded to
+    float32, z summed in float32, weighted sum in float64 rounded to float32.
+    """
+    y, x, _ = _check_qkv(q, k, v)
+    dev = _device()
+    f32 = q.dtype == np.float32
+    qd = torch.from_numpy(np.ascontiguousarray(q, dtype=np.float64)).to(dev)
+    kd = torch.from_numpy(np.ascontiguousarray(k, dtype=np.float64)).to(dev)
+    vd = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
+    s = qd @ kd.T
+    if f32:
+        s = s.float()
+    if scale != 1.0:
+        s = s * scale
+    if meter is not None:
+        meter.record(y * x)
+    name = getattr(spec, "name", None)
+    if name == "spherical":
+        w1, a2 = s, s * s
+    elif name == "signed_l1":
+        w1, a2 = s, s.abs()
+    elif name == "softmax":
+        w1 = a2 = torch.exp(s)
+    else:
+        raise ConfigError(f"unknown normaliser {name!r}")
+    z = a2.sum(dim=1)
+    ze = z + spec.denom_epsilon if spec.denom_epsilon else z
+    den = torch.sqrt(ze) if name == "spherical" else ze
+    bad = ~torch.isfinite(den) | (den == 0)
+    if y > 0 and bool(bad.any()):
+        row = int(torch.argmax(bad.to(torch.int8)))
+        raise DegenerateDenominatorError(float(z[row]), f"row {row}")
+    out = (w1 / den[:, None]).double() @ vd
+    return out.cpu().numpy().astype(_out_dtype(q), copy=False)
+
+
+def _dt(t):
+    return t.dtype if isinstance(t.dtype, str) else str(t.dtype)
+
+
+def naive_generalized_attention(q, k, v, cfg: AttentionConfig, meter: ScoreBufferMeter | None = None) -> DenseTensor:
+    """DenseTensor oracle wrapper (attention.py:282-298)."""
+    if not (_dt(q) == _dt(k) == _dt(v)):
+        raise ShapeMismatchError(f"dtype mismatch: {_dt(q)}, {_dt(k)}, {_dt(v)}")
+    qa, ka, va = q.array, k.array, v.array
+    if cfg.f16_emulation:
+        if _dt(q) != "float32":
+            raise ConfigError("f16 emulation requires float32 inputs")
+        qa, ka, va = (quantize_f16_array(a) for a in (qa, ka, va))
+    out = naive_attention_array(qa, ka, va, cfg.spec, cfg.resolve_scale(q.shape[1]), meter)
+    return DenseTensor(out, _dt(q), allow_nonfinite=cfg.f16_emulation)
+
+
+def streamed_attention(q, k, v, cfg: AttentionConfig, meter: ScoreBufferMeter | None = None) -> DenseTensor:
+    """DenseTensor fused-path wrapper (attention.py:301-315)."""
+    if not (_dt(q) == _dt(k) == _dt(v)):
+        raise ShapeMismatchError(f"dtype mismatch: {_dt(q)}, {_dt(k)}, {_dt(v)}")
+    out = streamed_attention_array(q.array, k.array, v.array, cfg.spec, cfg.resolve_scale(q.shape[1]),
+                                   cfg.tile, cfg.f16_emulation, meter)
+    return DenseTensor(out, _dt(q), allow_nonfinite=cfg.f16_emulation)
+
+
+def multi_head_attention(q, k, v, cfg: AttentionConfig, h: int, h_kv: int, path: str = "streamed",
+                         meter: ScoreBufferMeter | None = None) -> DenseTensor:
+    """DenseTensor multi-head wrapper (attention.py:364-378)."""
+    out = multi_head_attention_array(q.array, k.array, v.array, cfg.spec, h, h_kv, scale=cfg.score_scale,
+                                     tile=cfg.tile, path=path, f16=cfg.f16_emulation, meter=meter)
+    return DenseTensor(out, _dt(q))
+
+
+def apply_multiplicity_array(k: np.ndarray, m) -> np.ndarray:
+    """K'_i = m_i K_i (attention.py:381-388)."""
+    mv = np.asarray(m, dtype=np.float64)
+    if mv.ndim != 1 or mv.shape[0] != k.shape[0]:
+        raise ShapeMismatchError(f"multiplicity length {mv.shape} does not match {k.shape[0]} rows")
+    if not np.isfinite(mv).all() or (mv < 0).any():
+        raise ValueError("multiplicities must be finite and nonnegative")
+    return k * mv.astype(k.dtype).reshape((-1,) + (1,) * (k.ndim - 1))
+
+
+def apply_multiplicity(k, m) -> DenseTensor:
+    return DenseTensor(apply_multiplicity_array(k.array, m), _dt(k))

@@ -1,0 +1,155 @@
+"""Torch-native FlashSign forward: CUDA tensors in, CUDA tensor out, one launch.
+
+``fwd(q, k, v)`` takes BSHD tensors ``q [B, Nq, H, d]``, ``k, v [B, Nkv, H_kv, d]``
+(d contiguous, ``H % H_kv == 0``) in bf16 / fp16 / float8_e4m3fn and calls the
+C-ABI ``fs_fwd`` (include/flashsign.h) on the caller's current CUDA stream.
+It is the batched, device-resident form of the reference's
+``multi_head_attention_array`` (attention.py:318-361): every (batch, head,
+query tile) runs in one launch; query head h reads kv head h*H_kv//H
+(attention.py:352).
+
+Degenerate rows (b(z+eps) zero or non-finite, attention.py:196-199) are
+flagged on the device; ``check=True`` synchronises and raises
+``DegenerateDenominatorError`` for the first (batch, head, row) in the
+reference's loop order.  ``fwd_async`` returns the flag tensor instead of
+synchronising (benchmarks).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from ._errors import ConfigError
+from .normalizers import DegenerateDenominatorError
+from .tensor import ShapeMismatchError
+
+_IN_CODES = {torch.bfloat16: _lib.FS_BF16, torch.float16: _lib.FS_F16}
+if hasattr(torch, "float8_e4m3fn"):
+    _IN_CODES[torch.float8_e4m3fn] = _lib.FS_E4M3
+_OUT_CODES = {torch.float32: _lib.FS_F32, torch.bfloat16: _lib.FS_BF16, torch.float16: _lib.FS_F16}
+
+_STATUS_EXC = {
+    _lib.FS_ERR_SHAPE: ShapeMismatchError,
+    _lib.FS_ERR_DTYPE: ShapeMismatchError,
+    _lib.FS_ERR_CONFIG: ConfigError,
+    _lib.FS_ERR_UNSUPPORTED: ConfigError,
+    _lib.FS_ERR_CUDA: RuntimeError,
+}
+
+BAD_NONE = _lib.FS_BAD_NONE
+
+
+def _check_inputs(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not t.is_cuda:
+            raise RuntimeError(f"flashsign: {name} must be a CUDA tensor (no CPU fallback)")
+        if t.dim() != 4:
+            raise ShapeMismatchError(f"flashsign: {name} must be BSHD rank-4, got shape {tuple(t.shape)}")
+        if t.stride(-1) != 1:
+            raise ShapeMismatchError(f"flashsign: {name} head dim must be contiguous")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ShapeMismatchError(f"dtype mismatch: {q.dtype}, {k.dtype}, {v.dtype}")
+    if q.dtype not in _IN_CODES:
+        raise ShapeMismatchError(f"flashsign: unsupported input dtype {q.dtype} (bf16, fp16, float8_e4m3fn)")
+    b, _, _, d = q.shape
+    if k.shape[0] != b or v.shape[0] != b:
+        raise ShapeMismatchError(f"batch mismatch: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    if k.shape[3] != d:
+        raise ShapeMismatchError(f"Q and K feature dims differ: {tuple(q.shape)} vs {tuple(k.shape)}")
+    if v.shape[1] != k.shape[1] or v.shape[2] != k.shape[2]:
+        raise ShapeMismatchError(f"K and V shapes differ: {tuple(k.shape)} vs {tuple(v.shape)}")
+    if v.shape[3] != d:
+        raise ShapeMismatchError(f"flashsign: value dim must equal head dim ({v.shape[3]} vs {d})")
+    if q.device != k.device or q.device != v.device:
+        raise RuntimeError("flashsign: q, k, v must be on the same device")
+
+
+def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float = 1.0, eps: float = 0.0,
+              out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None, p_scale: float = 1.0,
+              q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0,
+              bad_key: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
+              tile_hint: tuple[int, int] = (0, 0)):
+    """Launch FlashSign and return ``(o, bad_key)`` without synchronising.
+
+    ``bad_key`` is a 1-element int64 CUDA tensor holding the packed first bad
+    row (see ``decode_bad_key``); it may be passed in to avoid an allocation.
+    """
+    _check_inputs(q, k, v)
+    if not math.isfinite(scale):
+        raise ConfigError(f"score_scale must be finite, got {scale}")
+    b, nq, h, d = q.shape
+    _, nkv, hkv, _ = k.shape
+    if h < 1 or hkv < 1 or h % hkv != 0:
+        raise ConfigError(f"query heads must be a multiple of kv heads, got h={h}, h_kv={hkv}")
+    if out_dtype is None:
+        out_dtype = out.dtype if out is not None else (torch.bfloat16 if q.dtype not in (torch.bfloat16, torch.float16)
+                                                       else q.dtype)
+    if out_dtype not in _OUT_CODES:
+        raise ShapeMismatchError(f"flashsign: unsupported output dtype {out_dtype}")
+    if out is None:
+        out = torch.empty((b, nq, h, d), dtype=out_dtype, device=q.device)
+    elif tuple(out.shape) != (b, nq, h, d) or out.dtype != out_dtype or out.stride(-1) != 1:
+        raise ShapeMismatchError(f"flashsign: bad out tensor {tuple(out.shape)} {out.dtype}")
+    if bad_key is None:
+        bad_key = torch.empty(1, dtype=torch.int64, device=q.device)
+
+    prm = _lib.FsFwdParams()
+    prm.q, prm.k, prm.v, prm.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
+    for dst, t in ((prm.q_stride, q), (prm.k_stride, k), (prm.v_stride, v), (prm.o_stride, out)):
+        dst[0], dst[1], dst[2] = t.stride(0), t.stride(1), t.stride(2)
+    prm.batch, prm.heads_q, prm.heads_kv = b, h, hkv
+    prm.seqlen_q, prm.seqlen_kv, prm.head_dim = nq, nkv, d
+    prm.in_dtype, prm.out_dtype = _IN_CODES[q.dtype], _OUT_CODES[out_dtype]
+    prm.scale, prm.eps, prm.p_scale = float(scale), float(eps), float(p_scale)
+    prm.q_descale, prm.k_descale, prm.v_descale = float(q_descale), float(k_descale), float(v_descale)
+    prm.bad_key = bad_key.data_ptr()
+    prm.tile_m_hint, prm.tile_n_hint = int(tile_hint[0]), int(tile_hint[1])
+
+    if stream is None:
+        with torch.cuda.device(q.device):
+            stream = torch.cuda.current_stream()
+    lib = _lib.load()
+    st = lib.fs_fwd(ctypes.byref(prm), ctypes.c_void_p(stream.cuda_stream))
+    if st != _lib.FS_OK:
+        raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
+    return out, bad_key
+
+
+def decode_bad_key(key: int, heads_q: int, seqlen_q: int):
+    """``None`` or ``(batch, head, row, z)`` for a packed bad-row key."""
+    key &= 0xFFFFFFFFFFFFFFFF
+    if key == BAD_NONE:
+        return None
+    lin = key >> 32
+    z = ctypes.c_float.from_buffer_copy(ctypes.c_uint32(key & 0xFFFFFFFF)).value
+    row = lin % seqlen_q
+    bh = lin // seqlen_q
+    return bh // heads_q, bh % heads_q, row, z
+
+
+def raise_if_bad(bad_key: torch.Tensor, heads_q: int, seqlen_q: int):
+    """Synchronise on ``bad_key`` and raise the reference's error for the first bad row."""
+    info = decode_bad_key(int(bad_key.item()), heads_q, seqlen_q)
+    if info is not None:
+        _, _, row, z = info
+        raise DegenerateDenominatorError(float(z), f"row {row}")
+
+
+def fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float = 1.0, eps: float = 0.0,
+        out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None, p_scale: float = 1.0,
+        q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0, check: bool = True) -> torch.Tensor:
+    """FlashSign forward ``O = c*sum_j s_ij v_j / sqrt(c^2 sum_j s_ij^2 + eps)`` on BSHD CUDA tensors."""
+    o, bad = fwd_async(q, k, v, scale=scale, eps=eps, out=out, out_dtype=out_dtype, p_scale=p_scale,
+                       q_descale=q_descale, k_descale=k_descale, v_descale=v_descale)
+    if check:
+        raise_if_bad(bad, q.shape[2], q.shape[1])
+    return o
+
+
+def flops(batch: int, heads: int, n_q: int, n_kv: int, d: int) -> int:
+    """Algorithmic FLOPs of one forward, 4*B*H*Nq*Nkv*d (costmodel.py:129)."""
+    return 4 * batch * heads * n_q * n_kv * d

@@ -1,0 +1,84 @@
+"""Batch x head sharding of FlashSign across GPUs (one process per GPU).
+
+The unit of work is one (batch element, kv-head group): u = b * H_kv + g.  A
+unit owns query heads [g*r, (g+1)*r) (r = H / H_kv) and kv head g of batch b.
+Units are independent -- disjoint (o, z) states, no cross-unit reduction
+(attention.py:351-360 runs heads independently) -- so ranks take
+contiguous unit ranges and the hot path needs no collective.  NCCL is used at
+most to gather O shards onto one rank (``gather_output``), timed separately.
+
+A unit range maps to at most one strided BSHD view per batch element it
+touches, so each rank issues ceil(units / H_kv) + 1 launches at most (one for
+the benchmark configurations, whose per-rank ranges align with batch rows).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+
+def unit_range(n_units: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) of units for ``rank``: sizes ceil/floor(n_units / world)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world {world}")
+    base, extra = divmod(n_units, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+@dataclass(frozen=True)
+class Piece:
+    """One launch worth of a rank's shard: batch b, kv heads [g0, g1)."""
+
+    b: int
+    g0: int
+    g1: int
+
+
+def pieces(batch: int, heads_kv: int, lo: int, hi: int) -> list[Piece]:
+    """Split unit range [lo, hi) into per-batch contiguous kv-head pieces."""
+    out = []
+    u = lo
+    while u < hi:
+        b, g = divmod(u, heads_kv)
+        g1 = min(heads_kv, g + (hi - u))
+        out.append(Piece(b, g, g1))
+        u += g1 - g
+    return out
+
+
+def piece_views(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, pc: Piece):
+    """Strided BSHD views (no copies) of one piece: q/o heads [g0*r, g1*r), k/v heads [g0, g1)."""
+    r = q.shape[2] // k.shape[2]
+    b = slice(pc.b, pc.b + 1)
+    return (q[b, :, pc.g0 * r: pc.g1 * r], k[b, :, pc.g0: pc.g1], v[b, :, pc.g0: pc.g1],
+            o[b, :, pc.g0 * r: pc.g1 * r])
+
+
+def fwd_shard(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, lo: int, hi: int, fwd, **kw):
+    """Run ``fwd(q_view, k_view, v_view, out=o_view, **kw)`` over units [lo, hi).
+
+    ``q/k/v/o`` are full-shape (or shard-local, with ``lo/hi`` relative to
+    them) BSHD tensors on this rank's device.  Returns the list of bad-key
+    tensors ``fwd`` produced (async; nothing synchronises here).
+    """
+    flags = []
+    for pc in pieces(q.shape[0], k.shape[2], lo, hi):
+        qv, kv_, vv, ov = piece_views(q, k, v, o, pc)
+        res = fwd(qv, kv_, vv, out=ov, **kw)
+        if isinstance(res, tuple):
+            flags.append(res[1])
+    return flags
+
+
+def gather_output(o_local: torch.Tensor, group=None) -> torch.Tensor:
+    """all_gather shard outputs (equal-size shards along batch) into one tensor on every rank."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = torch.empty((world * o_local.shape[0],) + tuple(o_local.shape[1:]), dtype=o_local.dtype,
+                      device=o_local.device)
+    dist.all_gather_into_tensor(out, o_local.contiguous(), group=group)
+    return out

@@ -1,0 +1,108 @@
+"""Pin the CPU oracle (oracle/spherical.py) against golden vectors produced by
+running the reference itself (tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle.spherical import (
+    OracleDegenerate,
+    gram_batched,
+    gram_spherical,
+    multi_head_spherical,
+    naive_spherical,
+    streamed_spherical,
+)
+
+
+def _args(g, c):
+    return g[f"{c}/q"], g[f"{c}/k"], g[f"{c}/v"], float(g[f"{c}/scale"]), float(g[f"{c}/eps"])
+
+
+def test_golden_has_cases(golden):
+    assert len(golden["__cases__"]) >= 20
+
+
+def test_kat_hand_exact(golden):
+    # test_attention.py:46-52 -- weights (0.6, 0.8): 0.6*10 + 0.8*20 = 22
+    for c in ("kat_hand", "kat_hand_streamed11", "kat_hand_f32"):
+        q, k, v, s, e = _args(golden, c)
+        assert golden[f"{c}/out"].tolist() == [[22.0]]
+        assert naive_spherical(q, k, v, s, e).tolist() == [[22.0]]
+        assert streamed_spherical(q, k, v, s, e, 1, 1).tolist() == [[22.0]]
+        assert streamed_spherical(q, k, v, s, e).tolist() == [[22.0]]
+
+
+def test_kat_sign_exact(golden):
+    for tag, sign in (("pos", 1.0), ("neg", -1.0)):
+        q, k, v, s, e = _args(golden, f"kat_sign_{tag}")
+        want = golden[f"kat_sign_{tag}/out"]
+        assert np.array_equal(want, sign * v)
+        assert np.array_equal(naive_spherical(q, k, v, s, e), want)
+        assert np.array_equal(streamed_spherical(q, k, v, s, e, 1, 1), want)
+
+
+@pytest.mark.parametrize("prefix", ["grid64", "grid32", "prime97", "c1", "scale_eps_mult"])
+def test_streamed_and_naive_match_reference(golden, prefix):
+    cases = [c for c in golden["__cases__"].tolist() if c.startswith(prefix)]
+    assert cases
+    for c in cases:
+        q, k, v, s, e = _args(golden, c)
+        want = golden[f"{c}/out"]
+        f32 = q.dtype == np.float32
+        rtol, atol = (1e-5, 1e-6) if f32 else (1e-12, 1e-14)
+        np.testing.assert_allclose(naive_spherical(q, k, v, s, e), want, rtol=rtol, atol=atol)
+        np.testing.assert_allclose(streamed_spherical(q, k, v, s, e), want, rtol=rtol, atol=atol)
+        for key, tile in (("streamed_13_7", (13, 7)), ("streamed_5_9", (5, 9))):
+            if f"{c}/{key}" in golden:
+                got = streamed_spherical(q, k, v, s, e, *tile)
+                # same tile + same precision policy as the reference -> tight agreement
+                np.testing.assert_allclose(got, golden[f"{c}/{key}"], rtol=rtol, atol=atol)
+
+
+@pytest.mark.parametrize("case", ["gqa_4_2", "gqa_2_1", "gqa_8_2_f32"])
+def test_multi_head_gqa_matches_reference(golden, case):
+    q, k, v, s, e = _args(golden, case)
+    h, hkv = int(golden[f"{case}/h"]), int(golden[f"{case}/h_kv"])
+    want = golden[f"{case}/out"]
+    f32 = q.dtype == np.float32
+    rtol, atol = (1e-5, 1e-6) if f32 else (1e-12, 1e-14)
+    np.testing.assert_allclose(multi_head_spherical(q, k, v, h, hkv, s, e), want, rtol=rtol, atol=atol)
+    # batched Gram oracle with the same GQA map (what the GPU tests use at full size)
+    got = gram_batched(q[None], k[None], v[None], s, e)[0]
+    np.testing.assert_allclose(got, want, rtol=1e-4 if f32 else 1e-10, atol=1e-5 if f32 else 1e-12)
+
+
+def test_f16_emulation_matches_reference(golden):
+    q, k, v, s, e = _args(golden, "f16_64")
+    got = streamed_spherical(q, k, v, s, e, 16, 16, f16=True)
+    np.testing.assert_array_equal(got, golden["f16_64/f16_out"])
+    # reference's own accuracy criterion (test_attention.py:351-357)
+    assert np.mean(np.abs(got - golden["f16_64/out"]) <= 0.01) >= 0.99
+
+
+def test_gram_identity_matches_reference_float64(golden):
+    for c in [c for c in golden["__cases__"].tolist() if c.startswith("grid64") or c == "prime97"]:
+        q, k, v, s, e = _args(golden, c)
+        np.testing.assert_allclose(gram_spherical(q, k, v, s, e), golden[f"{c}/out"], rtol=1e-9, atol=1e-12)
+
+
+def test_gram_criterion4(golden):
+    rng = np.random.default_rng(int(golden["crit4/seed"]))
+    q = rng.standard_normal((1024, 128)).astype(np.float32)
+    k = rng.standard_normal((1024, 128)).astype(np.float32)
+    v = rng.standard_normal((1024, 128)).astype(np.float32)
+    got = gram_spherical(q, k, v)
+    np.testing.assert_allclose(got, golden["crit4/out"], rtol=1e-4, atol=2e-6)
+
+
+@pytest.mark.parametrize("case", ["degen_row1", "degen_nan_row2", "degen_empty_k"])
+def test_degenerate_rows_match_reference(golden, case):
+    q, k, v, s, e = golden[f"{case}/q"], golden[f"{case}/k"], golden[f"{case}/v"], 1.0, 0.0
+    row = int(golden[f"{case}/err_row"])
+    z = float(golden[f"{case}/err_z"])
+    for fn in (lambda: naive_spherical(q, k, v, s, e), lambda: streamed_spherical(q, k, v, s, e),
+               lambda: streamed_spherical(q, k, v, s, e, 1, 1)):
+        with pytest.raises(OracleDegenerate) as ei:
+            fn()
+        assert ei.value.row == row
+        assert (np.isnan(z) and np.isnan(ei.value.z)) or ei.value.z == z
