@@ -1,0 +1,397 @@
+"""FlashSign forward benchmark (BASELINE.json metric: FlashSign fwd TFLOP/s and % of
+B200 tensor-core peak, 1-8 GPUs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step is one FlashSign forward over the rank's shard of the configuration
+(synthetic standard-normal Q/K/V, resident in HBM).  Work is sharded by
+(batch, kv-head) units with no collective (strong scaling: the configuration
+is fixed, ranks split it).  Timing: W warm-up steps, barrier +
+synchronize, CUDA events around exactly K steps on the launching stream,
+synchronize + barrier, MAX over ranks.  Rank 0 prints one JSON line.
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port of
+``_streamed_tiles``, oracle/spherical.py, tile 64x64, float32) on this host's
+cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs (C1 is the CPU-runnable correctness case, not a bench line)
+CONFIGS = {
+    "c2": dict(B=16, H=16, HKV=16, N=4096, D=64, dtype="fp16", eps=0.0, desc="B16 H16 N4096 d64 fp16"),
+    "c3": dict(B=8, H=16, HKV=16, N=16384, D=128, dtype="bf16", eps=0.0, desc="B8 H16 N16384 d128 bf16"),
+    "c4": dict(B=8, H=16, HKV=16, N=8192, D=128, dtype="e4m3", eps=0.0, desc="B8 H16 N8192 d128 e4m3 (bf16 out)"),
+    "c5": dict(B=64, H=8, HKV=8, N=20000, D=64, dtype="bf16", eps=1e-6,
+               desc="GRN B64 H8 N20000 d64 bf16, eps=1e-6, multiplicity-scaled K"),
+}
+PAPER_A100_TFLOPS = 200.0  # PAPER.md:199 (FlashSign fwd, d=128, FP16, A100) -- BASELINE.md section 1
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.02):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nvml is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_inputs(cfg, lo, hi, device, seed=1000):
+    """Shard [lo, hi) of (batch, kv-head) units as full-batch-row tensors.
+
+    Deterministic per unit: unit u's Q/K/V come from a generator seeded with
+    seed+u, so a shard's data equals the same units of a 1-GPU run.
+    Returns q, k, v for batch rows [b_lo, b_hi) and the unit offset.
+    """
+    import torch
+    B, H, HKV, N, D = cfg["B"], cfg["H"], cfg["HKV"], cfg["N"], cfg["D"]
+    b_lo, b_hi = lo // HKV, -(-hi // HKV)
+    r = H // HKV
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "e4m3": torch.float8_e4m3fn}[cfg["dtype"]]
+    nb = b_hi - b_lo
+    q = torch.empty((nb, N, H, D), dtype=tdt, device=device)
+    k = torch.empty((nb, N, HKV, D), dtype=tdt, device=device)
+    v = torch.empty((nb, N, HKV, D), dtype=tdt, device=device)
+    g = torch.Generator(device=device)
+    for u in range(max(lo, b_lo * HKV), min(hi, b_hi * HKV)):
+        b, hk = divmod(u, HKV)
+        g.manual_seed(seed + u)
+        bl = b - b_lo
+        q[bl, :, hk * r:(hk + 1) * r] = torch.randn((N, r, D), generator=g, device=device).to(tdt)
+        kk = torch.randn((N, D), generator=g, device=device)
+        if cfg.get("eps", 0.0) > 0:  # GRN: multiplicity-scaled keys, m in {0..5} (cli.py:296; grn.py:150)
+            m = torch.randint(0, 6, (N, 1), generator=g, device=device).float()
+            kk = kk * m
+        k[bl, :, hk] = kk.to(tdt)
+        v[bl, :, hk] = torch.randn((N, D), generator=g, device=device).to(tdt)
+    return q, k, v, b_lo * HKV
+
+
+def cpu_reference_sample(cfg, rows: int, seed: int = 7):
+    """Time the reference CPU algorithm (oracle port of _streamed_tiles, tile 64x64,
+    float32 inputs holding the dtype-quantised values) on ``rows`` query rows of one
+    (b, h) slice against all N keys.  Returns (seconds, flops, threads)."""
+    from oracle.spherical import streamed_spherical
+    threads = None
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"), default=None)
+    except Exception:
+        pass
+    rng = np.random.default_rng(seed)
+    N, D = cfg["N"], cfg["D"]
+    q = rng.standard_normal((rows, D)).astype(np.float32)
+    k = rng.standard_normal((N, D)).astype(np.float32)
+    v = rng.standard_normal((N, D)).astype(np.float32)
+    streamed_spherical(q[:64], k[:1024], v[:1024])  # warm-up
+    t0 = time.perf_counter()
+    streamed_spherical(q, k, v, 1.0, cfg.get("eps", 0.0), 64, 64)
+    dt = time.perf_counter() - t0
+    return dt, 4.0 * rows * N * D, threads or os.cpu_count()
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # reference arm: rank 0 only
+    rows = args.ref_rows
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, fl, threads = cpu_reference_sample(cfg, rows, seed=7 + i)
+        if i >= args.warmup:
+            times.append((dt, fl))
+    tot_t = sum(t for t, _ in times)
+    tot_f = sum(f for _, f in times)
+    val = tot_f / tot_t / 1e12
+    sample = (f"{rows} query rows x {cfg['N']} keys x d{cfg['D']} of one (b,h) slice per step, float32, "
+              f"tile 64x64 (oracle port of attention.py:146-200)")
+    line = {
+        "impl": "reference", "metric": "FlashSign fwd TFLOP/s", "value": val, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config, "desc": cfg["desc"], "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample,
+                         "cpu_count": os.cpu_count()},
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def context_baselines(cfg, q, k, v, device):
+    """PyTorch-eager spherical attention and SDPA softmax on the same GPU (one (b) row)."""
+    import torch
+    import torch.nn.functional as F
+    res = {}
+    if cfg["dtype"] == "e4m3":
+        q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
+    qb, kb, vb = q[:1], k[:1], v[:1]  # one batch row: [1, N, H, D]
+    H, N, D = qb.shape[2], qb.shape[1], qb.shape[3]
+    fl = 4.0 * H * N * N * D
+
+    def eager():  # per head to bound memory: S = q k^T ; O = (S v) / ||S||_row
+        for h in range(H):
+            hk = h * k.shape[2] // H
+            s = qb[0, :, h] @ kb[0, :, hk].T
+            z = s.float().square().sum(-1, keepdim=True).sqrt()
+            (s @ vb[0, :, hk]).float().div_(z)
+
+    def sdpa():
+        F.scaled_dot_product_attention(qb.transpose(1, 2), kb.transpose(1, 2), vb.transpose(1, 2))
+
+    for name, fn in (("torch_eager_spherical", eager), ("sdpa_softmax", sdpa)):
+        try:
+            fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 3
+            res[name] = {"tflops": fl / ms / 1e9, "ms_per_batch_row": ms, "dtype": str(qb.dtype)}
+        except Exception as ex:  # OOM etc. recorded, as the paper did
+            res[name] = {"error": f"{type(ex).__name__}: {str(ex)[:120]}"}
+    return res
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_09326_b200 import flashsign, partition
+    from paper_2505_09326_b200.pipeline import HostPipeline
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    B, H, HKV, N, D = cfg["B"], cfg["H"], cfg["HKV"], cfg["N"], cfg["D"]
+    n_units = B * HKV
+    lo, hi = partition.unit_range(n_units, world, rank)
+    q, k, v, u_off = make_inputs(cfg, lo, hi, dev)
+    out_dtype = torch.bfloat16 if cfg["dtype"] == "e4m3" else q.dtype
+    o = torch.empty(q.shape, dtype=out_dtype, device=dev)
+    r = H // HKV
+    my_flops = 4.0 * (hi - lo) * r * N * N * D
+    total_flops = 4.0 * B * H * N * N * D
+    kw = dict(scale=1.0, eps=cfg["eps"])
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def step():
+        return partition.fwd_shard(q, k, v, o, lo - u_off, hi - u_off,
+                                   lambda *a, **k2: flashsign.fwd_async(*a, bad_key=bad, **k2), **kw)
+
+    n_launch_per_step = len(partition.pieces(q.shape[0], HKV, lo - u_off, hi - u_off))
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    flashsign.raise_if_bad(bad, H, N) if cfg["eps"] == 0.0 else None
+
+    # ---------------- device-resident timed region
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = total_flops / (ms_step * 1e-3) / 1e12 if world > 1 else my_flops / (ms_step * 1e-3) / 1e12
+    kernel_ms = ms_step / n_launch_per_step  # one kernel launch per piece; back-to-back on one stream
+
+    # ---------------- end-to-end through the host-buffer API (pinned host in, host out)
+    e2e = None
+    if not args.no_e2e:
+        qh = q.cpu().pin_memory()
+        kh = k.cpu().pin_memory()
+        vh = v.cpu().pin_memory()
+        oh = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+        pipe = HostPipeline(dev)
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        for _ in range(min(args.warmup, 2)):
+            pipe.run(qh, kh, vh, oh, check=False, **kw)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            pipe.run(qh, kh, vh, oh, check=False, **kw)  # run() synchronises: output is on the host
+        dt = (time.perf_counter() - t0) / e2e_steps
+        tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        elsz = q.element_size()
+        h2d = (q.numel() + k.numel() + v.numel()) * elsz
+        d2h = o.numel() * o.element_size()
+        if world > 1:
+            vals = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
+            dist.all_reduce(vals)
+            h2d, d2h = int(vals[0].item()), int(vals[1].item())
+        e2e = {"value": (total_flops if world > 1 else my_flops) / dt / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
+               "steps": e2e_steps, "api": "paper_2505_09326_b200.pipeline.HostPipeline.run (pinned host bf16 in/out)"}
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        fp8 = cfg["dtype"] == "e4m3"
+        peak = peaks.get("fp8_tflops") if fp8 else peaks["bf16_tflops"]
+        peak_note = "MEASURED_PEAKS.json bf16_tflops (burst)"
+        if fp8 and peak is None:
+            peak = 2.0 * peaks["bf16_tflops"]
+            peak_note = "2 x MEASURED_PEAKS.json bf16_tflops (FP8 dense = 2x BF16; no measured FP8 peak)"
+        per_launch_flops = my_flops / n_launch_per_step
+        achieved = per_launch_flops / (kernel_ms * 1e-3) / 1e12
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get(args.config)
+        except Exception:
+            pass
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": f"{peak_src}: {peak_note}",
+                    "frac_of_sustained": (achieved / peaks["bf16_tflops_sustained"] / (2.0 if fp8 else 1.0))
+                    if "bf16_tflops_sustained" in peaks else None,
+                    "flops_per_launch": per_launch_flops, "kernel_ms": kernel_ms}
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            rows = args.cpu_rows or N
+            dt, fl, threads = cpu_reference_sample(cfg, rows)
+            cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                   "sample": f"{rows} query rows x {N} keys x d{D}, one (b,h) slice, float32, tile 64x64 "
+                             f"(oracle port of attention.py:146-200), {dt:.2f} s",
+                   "cpu_count": os.cpu_count()}
+        ctx = context_baselines(cfg, q, k, v, dev) if (world == 1 and args.context) else None
+        line = {
+            "metric": "FlashSign fwd TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": value / PAPER_A100_TFLOPS,
+            "vs_baseline_ref": "paper's A100 FlashSign fwd ~200 TFLOP/s (PAPER.md:199, BASELINE.md section 1)",
+            "dtype": {"bf16": "bf16", "fp16": "fp16", "e4m3": "e4m3"}[cfg["dtype"]], "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"], "batch": B, "heads": H, "heads_kv": HKV,
+                       "seq_len": N, "head_dim": D, "eps": cfg["eps"], "parallelism": f"batchxhead-shard{world}",
+                       "l2": "inputs larger than L2 (no flush needed)",
+                       "flops_per_step": total_flops},
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": n_launch_per_step * args.steps,
+            "roofline": roofline, "cpu_baseline": cpu,
+        }
+        if ctx is not None:
+            line["context"] = ctx
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-rows", type=int, default=512, help="query rows per CPU reference sample")
+    ap.add_argument("--cpu-rows", type=int, default=0, help="query rows of the cpu_baseline sample (0: one full slice)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--context", action="store_true", help="also time torch-eager spherical and SDPA")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

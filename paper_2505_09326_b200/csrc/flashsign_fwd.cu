@@ -40,6 +40,22 @@
 #include "../../include/flashsign.h"
 #include "sm100.cuh"
 
+#ifndef FS_VARIANT
+#define FS_VARIANT 0  // experiment knob (0 = production path)
+#endif
+#ifndef FS_TMA_ONCE
+#define FS_TMA_ONCE 0  // experiment: load the ring once, then reuse stale tiles
+#endif
+#ifndef FS_PURE_MMA
+#define FS_PURE_MMA 0  // experiment: MMA thread never waits on the norm warpgroups
+#endif
+#ifndef FS_SKIP_QK
+#define FS_SKIP_QK 0
+#endif
+#ifndef FS_SKIP_PV
+#define FS_SKIP_PV 0
+#endif
+
 namespace fs {
 
 constexpr int BM = 128;  // query rows per Q tile (= TMEM lanes)
@@ -238,6 +254,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int i = 0; i < 2 * n_kv_tiles; ++i) {
         const int slot = i % C::STAGES;
         const int round = i / C::STAGES;
+        if (FS_TMA_ONCE && round > 0) break;
         if (round > 0) ptx::mbar_wait(&bars->kv_empty[slot], (round - 1) & 1);
         ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::SLOT_BYTES);
         const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
@@ -251,73 +268,99 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && n_kv_tiles > 0) {
-      const uint32_t q_base = smem_s;
-      const uint32_t ring_base = smem_s + C::RING_OFF;
+    // The whole warp runs the (warp-uniform) control flow and waits; one elected
+    // lane issues.  Descriptors are built once; per-step offsets are constants, so
+    // every MMA is a couple of uniform-register adds (~64 cycles of tensor work each).
+    if (n_kv_tiles > 0) {
+      const bool leader = ptx::elect_one();
+      const uint64_t q_desc = ptx::sdesc_sw128(smem_s, 16, 1024);
+      const uint64_t k_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, 16, 1024);
+      const uint64_t v_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, BN * 128, 1024);
       auto qk = [&](int t, int slot) {
-        const uint32_t a0 = q_base + t * C::Q_TILE_BYTES;
-        const uint32_t b0 = ring_base + slot * C::SLOT_BYTES;
+        if (FS_SKIP_QK) return;
+        const uint64_t a0 = q_desc + static_cast<uint32_t>((t * C::Q_TILE_BYTES) >> 4);
+        const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
         const uint32_t d_tmem = tmem + C::COL_S0 + t * BN;
 #pragma unroll
         for (int ks = 0; ks < C::QK_STEPS; ++ks) {
-          const uint32_t off_a = (ks * 32 / 128) * (BM * 128) + (ks * 32) % 128;
-          const uint32_t off_b = (ks * 32 / 128) * (BN * 128) + (ks * 32) % 128;
-          const uint64_t ad = ptx::sdesc_sw128(a0 + off_a, 16, 1024);
-          const uint64_t bd = ptx::sdesc_sw128(b0 + off_b, 16, 1024);
+          const uint32_t off_a = ((ks * 32 / 128) * (BM * 128) + (ks * 32) % 128) >> 4;
+          const uint32_t off_b = ((ks * 32 / 128) * (BN * 128) + (ks * 32) % 128) >> 4;
           if constexpr (TR::F8)
-            ptx::mma_f8_ss(d_tmem, ad, bd, C::IDESC_QK, ks > 0);
+            ptx::mma_f8_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
           else
-            ptx::mma_f16_ss(d_tmem, ad, bd, C::IDESC_QK, ks > 0);
+            ptx::mma_f16_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
         }
       };
       auto pv = [&](int t, int slot, bool acc) {
-        const uint32_t b0 = ring_base + slot * C::SLOT_BYTES;
+        if (FS_SKIP_PV) return;
+        const uint64_t b0 = v_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
         const uint32_t a_tmem = tmem + C::COL_S0 + t * BN;
         const uint32_t d_tmem = tmem + C::COL_O0 + t * D;
 #pragma unroll
         for (int ks = 0; ks < C::PV_STEPS; ++ks) {
-          const uint64_t bd = ptx::sdesc_sw128(b0 + ks * TR::KSTEP * 128, BN * 128, 1024);
+          const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
           const uint32_t at = a_tmem + ks * (TR::KSTEP * C::EB / 4);
           if constexpr (TR::F8)
-            ptx::mma_f8_ts(d_tmem, at, bd, C::IDESC_PV, (acc || ks > 0) ? 1u : 0u);
+            ptx::mma_f8_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, (acc || ks > 0) ? 1u : 0u);
           else
-            ptx::mma_f16_ts(d_tmem, at, bd, C::IDESC_PV, (acc || ks > 0) ? 1u : 0u);
+            ptx::mma_f16_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, (acc || ks > 0) ? 1u : 0u);
         }
       };
 #pragma unroll
       for (int t = 0; t < NQT; ++t) ptx::mbar_wait(&bars->q_full[t], 0);
       ptx::tc_fence_after();
+      // ring position of K_j (even loads) and V_j (odd loads)
+      int k_slot = 0, k_phase = 0;
+      int v_slot = 1 % C::STAGES, v_phase = (1 >= C::STAGES) ? 1 : 0;
       int prev_v_slot = 0;
       for (int j = 0; j < n_kv_tiles; ++j) {
-        const int ik = 2 * j, iv = 2 * j + 1;
-        const int k_slot = ik % C::STAGES, v_slot = iv % C::STAGES;
-        ptx::mbar_wait(&bars->kv_full[k_slot], (ik / C::STAGES) & 1);
+        if (!FS_TMA_ONCE || 2 * j < C::STAGES) ptx::mbar_wait(&bars->kv_full[k_slot], k_phase);
         ptx::tc_fence_after();
-        qk(0, k_slot);
-        ptx::tc_commit(&bars->s_full[0]);
-        if (j > 0) {
-          ptx::mbar_wait(&bars->p_full[1], (j - 1) & 1);
-          ptx::tc_fence_after();
-          pv(1, prev_v_slot, j - 1 > 0);
-          ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
+        if (leader) {
+          qk(0, k_slot);
+          ptx::tc_commit(&bars->s_full[0]);
         }
-        qk(1, k_slot);
-        ptx::tc_commit(&bars->s_full[1]);
-        ptx::tc_commit(&bars->kv_empty[k_slot]);
-        ptx::mbar_wait(&bars->kv_full[v_slot], (iv / C::STAGES) & 1);
-        ptx::mbar_wait(&bars->p_full[0], j & 1);
+        __syncwarp();
+        if (j > 0) {
+          if (!FS_PURE_MMA) ptx::mbar_wait(&bars->p_full[1], (j - 1) & 1);
+          ptx::tc_fence_after();
+          if (leader) {
+            pv(1, prev_v_slot, j - 1 > 0);
+            ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
+          }
+          __syncwarp();
+        }
+        if (leader) {
+          qk(1, k_slot);
+          ptx::tc_commit(&bars->s_full[1]);
+          ptx::tc_commit(&bars->kv_empty[k_slot]);
+        }
+        __syncwarp();
+        if (!FS_TMA_ONCE || 2 * j + 1 < C::STAGES) ptx::mbar_wait(&bars->kv_full[v_slot], v_phase);
+        if (!FS_PURE_MMA) ptx::mbar_wait(&bars->p_full[0], j & 1);
         ptx::tc_fence_after();
-        pv(0, v_slot, j > 0);
-        if (j == n_kv_tiles - 1) ptx::tc_commit(&bars->o_full[0]);
+        if (leader) {
+          pv(0, v_slot, j > 0);
+          if (j == n_kv_tiles - 1) ptx::tc_commit(&bars->o_full[0]);
+        }
+        __syncwarp();
         prev_v_slot = v_slot;
+        // advance both ring cursors by two loads
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          if (++k_slot == C::STAGES) { k_slot = 0; k_phase ^= 1; }
+          if (++v_slot == C::STAGES) { v_slot = 0; v_phase ^= 1; }
+        }
       }
-      ptx::mbar_wait(&bars->p_full[1], (n_kv_tiles - 1) & 1);
+      if (!FS_PURE_MMA) ptx::mbar_wait(&bars->p_full[1], (n_kv_tiles - 1) & 1);
       ptx::tc_fence_after();
-      pv(1, prev_v_slot, n_kv_tiles - 1 > 0);
-      ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
-      ptx::tc_commit(&bars->o_full[1]);
+      if (leader) {
+        pv(1, prev_v_slot, n_kv_tiles - 1 > 0);
+        ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
+        ptx::tc_commit(&bars->o_full[1]);
+      }
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ norm warpgroups
     const int t = (warp - 4) >> 2;  // Q tile owned by this warpgroup
@@ -329,15 +372,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const float ps = p.p_scale;
     float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
     float amax = 0.f;
-    for (int j = 0; j < n_kv_tiles; ++j) {
+    for (int j = 0; j < (FS_PURE_MMA ? 0 : n_kv_tiles); ++j) {
       ptx::mbar_wait(&bars->s_full[t], j & 1);
       ptx::tc_fence_after();
+#if FS_VARIANT == 3
+      // experiment: no TMEM traffic at all
+#elif FS_VARIANT == 5
+      {
+        uint32_t s[128];
+        ptx::tmem_ld32(s_addr + 0, s);
+        ptx::tmem_ld32(s_addr + 32, s + 32);
+        ptx::tmem_ld32(s_addr + 64, s + 64);
+        ptx::tmem_ld32(s_addr + 96, s + 96);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 128; i += 4) {
+          const float a = __uint_as_float(s[i]), b = __uint_as_float(s[i + 1]);
+          const float c = __uint_as_float(s[i + 2]), d = __uint_as_float(s[i + 3]);
+          z0 = fmaf(a, a, z0);
+          z1 = fmaf(b, b, z1);
+          z2 = fmaf(c, c, z2);
+          z3 = fmaf(d, d, z3);
+        }
+        if constexpr (!TR::F8) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) s[i] = pack2<IN>(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
+          ptx::tmem_st32(s_addr, s);
+          ptx::tmem_st32(s_addr + 32, s + 32);
+        }
+      }
+#else
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         uint32_t s[64];
+#if FS_VARIANT == 1
+#pragma unroll
+        for (int i = 0; i < 64; ++i) s[i] = __float_as_uint((float)(lane + i));
+#else
         ptx::tmem_ld32(s_addr + half * 64, s);
         ptx::tmem_ld32(s_addr + half * 64 + 32, s + 32);
         ptx::tmem_wait_ld();
+#endif
+#if FS_VARIANT != 2
 #pragma unroll
         for (int i = 0; i < 64; i += 4) {
           const float a = __uint_as_float(s[i]), b = __uint_as_float(s[i + 1]);
@@ -367,7 +443,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           ptx::tmem_st32(s_addr + half * 32, pk);
         }
+#else
+        z0 += __uint_as_float(s[half]);
+#endif
       }
+#endif
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();

@@ -7,9 +7,9 @@ Units are independent -- disjoint (o, z) states, no cross-unit reduction
 contiguous unit ranges and the hot path needs no collective.  NCCL is used at
 most to gather O shards onto one rank (``gather_output``), timed separately.
 
-A unit range maps to at most one strided BSHD view per batch element it
-touches, so each rank issues ceil(units / H_kv) + 1 launches at most (one for
-the benchmark configurations, whose per-rank ranges align with batch rows).
+A unit range becomes at most three launches: a partial leading batch row, a
+block of whole batch rows (one launch), and a partial trailing row.  Each is a
+strided BSHD view of the full tensors, so no data moves.
 """
 
 from __future__ import annotations
@@ -30,29 +30,40 @@ def unit_range(n_units: int, world: int, rank: int) -> tuple[int, int]:
 
 @dataclass(frozen=True)
 class Piece:
-    """One launch worth of a rank's shard: batch b, kv heads [g0, g1)."""
+    """One launch: batch rows [b0, b1) x kv heads [g0, g1) (g-range partial only if b1 == b0 + 1)."""
 
-    b: int
+    b0: int
+    b1: int
     g0: int
     g1: int
 
 
 def pieces(batch: int, heads_kv: int, lo: int, hi: int) -> list[Piece]:
-    """Split unit range [lo, hi) into per-batch contiguous kv-head pieces."""
-    out = []
+    """Cover unit range [lo, hi) with at most three rectangular pieces."""
+    if not 0 <= lo <= hi <= batch * heads_kv:
+        raise ValueError(f"unit range [{lo}, {hi}) outside [0, {batch * heads_kv})")
+    out: list[Piece] = []
     u = lo
-    while u < hi:
+    if u < hi and u % heads_kv:
         b, g = divmod(u, heads_kv)
         g1 = min(heads_kv, g + (hi - u))
-        out.append(Piece(b, g, g1))
+        out.append(Piece(b, b + 1, g, g1))
         u += g1 - g
+    full = (hi - u) // heads_kv
+    if full:
+        b = u // heads_kv
+        out.append(Piece(b, b + full, 0, heads_kv))
+        u += full * heads_kv
+    if u < hi:
+        b = u // heads_kv
+        out.append(Piece(b, b + 1, 0, hi - u))
     return out
 
 
 def piece_views(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, pc: Piece):
     """Strided BSHD views (no copies) of one piece: q/o heads [g0*r, g1*r), k/v heads [g0, g1)."""
     r = q.shape[2] // k.shape[2]
-    b = slice(pc.b, pc.b + 1)
+    b = slice(pc.b0, pc.b1)
     return (q[b, :, pc.g0 * r: pc.g1 * r], k[b, :, pc.g0: pc.g1], v[b, :, pc.g0: pc.g1],
             o[b, :, pc.g0 * r: pc.g1 * r])
 
@@ -60,9 +71,9 @@ def piece_views(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tens
 def fwd_shard(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, lo: int, hi: int, fwd, **kw):
     """Run ``fwd(q_view, k_view, v_view, out=o_view, **kw)`` over units [lo, hi).
 
-    ``q/k/v/o`` are full-shape (or shard-local, with ``lo/hi`` relative to
-    them) BSHD tensors on this rank's device.  Returns the list of bad-key
-    tensors ``fwd`` produced (async; nothing synchronises here).
+    ``q/k/v/o`` are BSHD tensors on this rank's device (``lo/hi`` are unit
+    indices relative to them).  Returns the bad-key tensors ``fwd`` produced
+    (async; nothing synchronises here).
     """
     flags = []
     for pc in pieces(q.shape[0], k.shape[2], lo, hi):
@@ -74,7 +85,7 @@ def fwd_shard(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor
 
 
 def gather_output(o_local: torch.Tensor, group=None) -> torch.Tensor:
-    """all_gather shard outputs (equal-size shards along batch) into one tensor on every rank."""
+    """all_gather equal-size shard outputs (along batch) into one tensor on every rank."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)

@@ -1,0 +1,190 @@
+"""CPU-only tests of the drop-in boundary: the C-ABI library loads and exports every
+symbol include/flashsign.h declares, its struct layout matches the header, host
+validation maps to the reference's exception types, and the ncstream-compatible
+API rejects bad input exactly like the reference -- all without a GPU."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2505_09326_b200 import _lib, flashsign
+from paper_2505_09326_b200.attention import (
+    AttentionConfig,
+    ConfigError,
+    TileConfig,
+    default_score_scale,
+    multi_head_attention_array,
+    streamed_attention,
+    streamed_attention_array,
+)
+from paper_2505_09326_b200.normalizers import SIGNED_L1, SOFTMAX, SPHERICAL, DegenerateDenominatorError
+from paper_2505_09326_b200.tensor import DenseTensor, ShapeMismatchError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "flashsign.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*[a-z_ ]+\**\s*\*?\s*(fs_[a-z_]+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = header_functions()
+    assert set(names) == set(_lib.EXPORTED_SYMBOLS)
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}$", out, re.M), f"{n} not exported"
+
+
+def test_library_is_sm100a_with_tcgen05():
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in sass
+    for mnem in ("UTCHMMA", "UTCQMMA", "UTMALDG", "LDTM", "STTM"):
+        assert mnem in sass, mnem
+    assert "HMMA" not in re.sub(r"UTC[HQ]MMA", "", sass)  # no legacy mma.sync path
+
+
+def test_struct_layout_matches_header(tmp_path):
+    fields = [f[0] for f in _lib.FsFwdParams._fields_]
+    prog = tmp_path / "layout.c"
+    body = "\n".join(f'printf("{f} %zu\\n", offsetof(fs_fwd_params, {f}));' for f in fields)
+    prog.write_text(f'#include <stdio.h>\n#include <stddef.h>\n#include "{HEADER}"\nint main(void){{\n'
+                    f'printf("size %zu\\n", sizeof(fs_fwd_params));\n{body}\nreturn 0;}}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c99", str(prog), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    assert int(got["size"]) == ctypes.sizeof(_lib.FsFwdParams)
+    for f in fields:
+        assert int(got[f]) == getattr(_lib.FsFwdParams, f).offset, f
+
+
+def _params(**kw):
+    p = _lib.FsFwdParams()
+    p.batch, p.heads_q, p.heads_kv, p.seqlen_q, p.seqlen_kv, p.head_dim = 1, 4, 2, 128, 128, 64
+    p.in_dtype, p.out_dtype = _lib.FS_BF16, _lib.FS_BF16
+    p.scale, p.eps, p.p_scale, p.q_descale, p.k_descale, p.v_descale = 1.0, 0.0, 1.0, 1.0, 1.0, 1.0
+    p.q = p.k = p.v = p.o = 1 << 20
+    for s in (p.q_stride, p.k_stride, p.v_stride, p.o_stride):
+        s[0], s[1], s[2] = 128 * 4 * 64, 4 * 64, 64
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+@pytest.mark.parametrize("kw,status,needle", [
+    (dict(heads_q=3, heads_kv=2), _lib.FS_ERR_CONFIG, "multiple"),
+    (dict(head_dim=200), _lib.FS_ERR_UNSUPPORTED, "head_dim"),
+    (dict(head_dim=4), _lib.FS_ERR_UNSUPPORTED, "multiple of 16"),
+    (dict(in_dtype=_lib.FS_F32), _lib.FS_ERR_DTYPE, "in_dtype"),
+    (dict(scale=float("nan")), _lib.FS_ERR_CONFIG, "finite"),
+    (dict(eps=-1.0), _lib.FS_ERR_CONFIG, "epsilon"),
+    (dict(p_scale=0.0), _lib.FS_ERR_CONFIG, "positive"),
+    (dict(heads_q=0), _lib.FS_ERR_SHAPE, "extents"),
+    (dict(q=(1 << 20) + 8), _lib.FS_ERR_UNSUPPORTED, "aligned"),
+])
+def test_fs_fwd_validation(kw, status, needle):
+    lib = _lib.load()
+    st = lib.fs_fwd(ctypes.byref(_params(**kw)), None)
+    assert st == status
+    assert needle in _lib.last_error()
+
+
+def test_query_tile():
+    assert _lib.query_tile(64, _lib.FS_BF16) == (128, 128)
+    assert _lib.query_tile(128, _lib.FS_E4M3) == (128, 128)
+    with pytest.raises(ValueError):
+        _lib.query_tile(0, _lib.FS_BF16)
+
+
+def test_bad_key_decoding():
+    lin = (2 * 8 + 5) * 300 + 17  # batch 2, head 5 of 8, row 17 of 300
+    z = np.float32(0.0)
+    key = (lin << 32) | int(np.array([z]).view(np.uint32)[0])
+    assert flashsign.decode_bad_key(key, 8, 300) == (2, 5, 17, 0.0)
+    assert flashsign.decode_bad_key(_lib.FS_BAD_NONE, 8, 300) is None
+    key_nan = (3 << 32) | 0x7FC00000
+    b, h, row, zz = flashsign.decode_bad_key(key_nan, 1, 10)
+    assert (b, h, row) == (0, 0, 3) and np.isnan(zz)
+    # ordering of packed keys == reference loop order (batch, head, row)
+    keys = [((bb * 4 + hh) * 10 + rr) << 32 for bb in range(2) for hh in range(4) for rr in range(10)]
+    assert keys == sorted(keys)
+
+
+# ---------------------------------------------------------------- compat API (validation paths only)
+
+def test_compat_shape_errors_match_reference():
+    with pytest.raises(ShapeMismatchError):
+        streamed_attention_array(np.ones((2, 3)), np.ones((2, 4)), np.ones((2, 4)), SPHERICAL, 1.0, TileConfig())
+    with pytest.raises(ShapeMismatchError):
+        streamed_attention_array(np.ones((2, 3, 1)), np.ones((2, 3)), np.ones((2, 3)), SPHERICAL, 1.0, TileConfig())
+    with pytest.raises(ShapeMismatchError):
+        streamed_attention_array(np.ones((2, 3)), np.ones((4, 3)), np.ones((5, 3)), SPHERICAL, 1.0, TileConfig())
+
+
+def test_compat_config_errors_match_reference():
+    # test_attention.py:275-278
+    with pytest.raises(ConfigError, match="multiple"):
+        multi_head_attention_array(np.ones((2, 3, 2)), np.ones((2, 2, 2)), np.ones((2, 2, 2)), SPHERICAL, h=3, h_kv=2)
+    with pytest.raises(ConfigError):
+        multi_head_attention_array(np.ones((2, 2, 2)), np.ones((2, 1, 2)), np.ones((2, 1, 2)), SPHERICAL, 2, 1,
+                                   path="bogus")
+    with pytest.raises(ShapeMismatchError):
+        multi_head_attention_array(np.ones((2, 2)), np.ones((2, 1, 2)), np.ones((2, 1, 2)), SPHERICAL, 2, 1)
+    with pytest.raises(ConfigError):
+        TileConfig(0, 4)
+    with pytest.raises(ConfigError):
+        AttentionConfig(SPHERICAL, score_scale=0.0)
+    with pytest.raises(ConfigError):
+        AttentionConfig(SPHERICAL, score_scale=float("nan"))
+    # test_attention.py:340-344: f16 emulation needs float32
+    q = DenseTensor(np.ones((2, 2)))
+    with pytest.raises(ConfigError, match="float32"):
+        streamed_attention(q, q, q, AttentionConfig(SPHERICAL, f16_emulation=True))
+
+
+def test_compat_non_spherical_rejected_on_streamed_path():
+    for spec in (SOFTMAX, SIGNED_L1):
+        with pytest.raises(ConfigError, match="spherical"):
+            streamed_attention_array(np.ones((2, 8), np.float32), np.ones((2, 8), np.float32),
+                                     np.ones((2, 8), np.float32), spec, 1.0, TileConfig())
+
+
+def test_default_scales_match_reference():
+    # test_attention.py:321-325
+    assert default_score_scale(SOFTMAX, 64) == 64 ** -0.5
+    assert default_score_scale(SPHERICAL, 64) == 1.0
+    assert default_score_scale(SIGNED_L1, 64) == 1.0
+    assert AttentionConfig(SOFTMAX).resolve_scale(16) == 0.25
+    assert AttentionConfig(SOFTMAX, score_scale=2.0).resolve_scale(16) == 2.0
+
+
+def test_degenerate_error_message_matches_reference():
+    e = DegenerateDenominatorError(0.0, "row 1")
+    assert "row 1" in str(e) and e.z == 0.0 and isinstance(e, ValueError)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError, match="CUDA"):
+        streamed_attention_array(np.ones((4, 8), np.float32), np.ones((4, 8), np.float32),
+                                 np.ones((4, 8), np.float32), SPHERICAL, 1.0, TileConfig())
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2505_09326_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|\"\"\".*?\"\"\"", "", src, flags=re.S).replace(
+                    "oracle/", ""), f"{f} references the oracle"
