@@ -611,6 +611,19 @@ static fs_status dispatch_out(const fs_fwd_params* p, cudaStream_t s) {
 
 }  // namespace fs
 
+static fs_status fs_fwd_dispatch(const fs_fwd_params* p, cudaStream_t stream) {
+  using namespace fs;
+
+  if (p->in_dtype == FS_E4M3) {
+    // 1-byte rows: the SW128 layout needs 128-byte rows -> D = 128 (TMA zero-fills d >= head_dim).
+    return dispatch_out<FS_E4M3, 128>(p, stream);
+  }
+  const bool d64 = p->head_dim <= 64;
+  if (p->in_dtype == FS_BF16) return d64 ? dispatch_out<FS_BF16, 64>(p, stream) : dispatch_out<FS_BF16, 128>(p, stream);
+  return d64 ? dispatch_out<FS_F16, 64>(p, stream) : dispatch_out<FS_F16, 128>(p, stream);
+}
+
+
 extern "C" {
 
 const char* fs_last_error(void) { return fs::g_last_error.c_str(); }
@@ -650,7 +663,7 @@ fs_status fs_fwd(const fs_fwd_params* p, fs_stream_t stream_) {
     return fail(FS_ERR_UNSUPPORTED, "head_dim * elem_bytes must be a multiple of 16 (pad the head dim)");
   if (p->heads_q > 65535 || p->batch > 65535) return fail(FS_ERR_UNSUPPORTED, "heads/batch must be <= 65535");
   auto aligned16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
-  if (!aligned16(p->q) || !aligned16(p->k) || !aligned16(p->v) || !aligned16(p->o))
+  if (!aligned16(p->q) || !aligned16(p->k) || !aligned16(p->v) || !aligned16(p->o))  // NULL is aligned
     return fail(FS_ERR_UNSUPPORTED, "q/k/v/o must be 16-byte aligned");
   for (int i = 0; i < 3; ++i) {
     if ((p->q_stride[i] * eb) % 16 || (p->k_stride[i] * eb) % 16 || (p->v_stride[i] * eb) % 16 ||
@@ -662,15 +675,18 @@ fs_status fs_fwd(const fs_fwd_params* p, fs_stream_t stream_) {
     if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
   }
   if (p->batch == 0 || p->seqlen_q == 0) return FS_OK;
-  if (!p->q || !p->k || !p->v || !p->o) return fail(FS_ERR_CONFIG, "null tensor pointer");
-
-  if (p->in_dtype == FS_E4M3) {
-    // 1-byte rows: the SW128 layout needs 128-byte rows -> D = 128 (TMA zero-fills d >= head_dim).
-    return dispatch_out<FS_E4M3, 128>(p, stream);
+  if (!p->q || !p->o || (p->seqlen_kv > 0 && (!p->k || !p->v))) return fail(FS_ERR_CONFIG, "null tensor pointer");
+  if (p->seqlen_kv == 0) {
+    // Empty K/V stream: nothing is loaded, every row has z = 0.  The TMA maps still need a
+    // valid global address, so describe K/V over q's storage (never dereferenced).
+    fs_fwd_params p2 = *p;
+    p2.k = p2.v = p->q;
+    for (int i = 0; i < 3; ++i) p2.k_stride[i] = p2.v_stride[i] = p->q_stride[i];
+    p2.heads_kv = p->heads_q;
+    p2.seqlen_kv = 0;
+    return fs_fwd_dispatch(&p2, stream);
   }
-  const bool d64 = p->head_dim <= 64;
-  if (p->in_dtype == FS_BF16) return d64 ? dispatch_out<FS_BF16, 64>(p, stream) : dispatch_out<FS_BF16, 128>(p, stream);
-  return d64 ? dispatch_out<FS_F16, 64>(p, stream) : dispatch_out<FS_F16, 128>(p, stream);
+  return fs_fwd_dispatch(p, stream);
 }
 
 }  // extern "C"
