@@ -89,7 +89,12 @@ def gather_output(o_local: torch.Tensor, group=None) -> torch.Tensor:
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    out = torch.empty((world * o_local.shape[0],) + tuple(o_local.shape[1:]), dtype=o_local.dtype,
-                      device=o_local.device)
-    dist.all_gather_into_tensor(out, o_local.contiguous(), group=group)
-    return out
+    o_local = o_local.contiguous()
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world * o_local.shape[0],) + tuple(o_local.shape[1:]), dtype=o_local.dtype,
+                          device=o_local.device)
+        dist.all_gather_into_tensor(out, o_local, group=group)
+        return out
+    parts = [torch.empty_like(o_local) for _ in range(world)]
+    dist.all_gather(parts, o_local, group=group)
+    return torch.cat(parts, dim=0)

@@ -106,3 +106,35 @@ def test_degenerate_rows_match_reference(golden, case):
             fn()
         assert ei.value.row == row
         assert (np.isnan(z) and np.isnan(ei.value.z)) or ei.value.z == z
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REF_SRC), reason="reference not mounted (GPU box)")
+def test_oracle_port_bitwise_equals_live_reference():
+    """The CPU baseline (oracle port of _streamed_tiles) is the reference's algorithm:
+    bitwise-identical outputs to ncstream.attention.streamed_attention_array, run live."""
+    import sys
+    sys.path.insert(0, REF_SRC)
+    try:
+        from ncstream.attention import TileConfig, multi_head_attention_array, streamed_attention_array
+        from ncstream.normalizers import SPHERICAL
+    finally:
+        sys.path.remove(REF_SRC)
+    rng = np.random.default_rng(11)
+    for (y, x, d, dt, tile, scale, eps) in [(300, 517, 64, np.float32, (64, 64), 1.0, 0.0),
+                                           (97, 33, 8, np.float64, (13, 7), -0.7, 1e-6),
+                                           (128, 256, 128, np.float32, (16, 32), 2.0, 0.0)]:
+        q, k, v = (rng.standard_normal(s).astype(dt) for s in ((y, d), (x, d), (x, d)))
+        want = streamed_attention_array(q, k, v, SPHERICAL.with_epsilon(eps), scale, TileConfig(*tile))
+        got = streamed_spherical(q, k, v, scale, eps, *tile)
+        assert np.array_equal(got, want)
+    q = rng.standard_normal((50, 4, 16)).astype(np.float32)
+    k = rng.standard_normal((70, 2, 16)).astype(np.float32)
+    v = rng.standard_normal((70, 2, 16)).astype(np.float32)
+    assert np.array_equal(multi_head_spherical(q, k, v, 4, 2),
+                          multi_head_attention_array(q, k, v, SPHERICAL, 4, 2))
+    f = rng.standard_normal((64, 16)).astype(np.float32)
+    assert np.array_equal(streamed_spherical(f, f, f, 1.0, 0.0, 16, 16, f16=True),
+                          streamed_attention_array(f, f, f, SPHERICAL, 1.0, TileConfig(16, 16), f16=True))
