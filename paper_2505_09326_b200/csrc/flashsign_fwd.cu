@@ -5,20 +5,26 @@
 // (attention.py:252-279, 318-361).  Contract (normalizers.py:94-100):
 //     O_i = c * sum_j s_ij v_j / sqrt(c^2 * sum_j s_ij^2 + eps),   s_ij = q_i . k_j
 //
-// One CTA owns NQT=2 query tiles of BM=128 rows of one (batch, head) and streams
-// the K/V tiles of that head's kv-group through a TMA-fed shared-memory ring:
+// Persistent kernel: one CTA per SM walks work tiles (batch, head, 256 query rows =
+// NQT=2 query tiles of BM=128) with a static stride.  Roles (512 threads):
 //
-//   warp 0      TMA producer   Q tiles once, then K_j, V_j into a STAGES-deep ring
-//   warp 1      MMA issuer     S_t = Q_t K_j^T  (tcgen05 SS, S in TMEM, fp32)
-//                              O_t += P_t V_j   (tcgen05 TS: P read from TMEM, V MN-major)
-//   warp 2      TMEM allocator (512 columns: O_0, O_1, S_0, S_1)
-//   warps 4-7   norm WG 0      row r of tile 0: z += sum s^2 (registers), P = cvt(s) -> TMEM
-//   warps 8-11  norm WG 1      same for tile 1, ping-ponging with WG 0
+//   warp 0       TMA producer   Q tiles of the next work tile as soon as their buffer frees,
+//                               K_j / V_j into a STAGES-deep ring that runs across work tiles
+//   warp 1       MMA issuer     S_t = Q_t K_j^T  (tcgen05 SS, S in TMEM, fp32)
+//                               O_t += P_t V_j   (tcgen05 TS: P read from TMEM, V MN-major),
+//                               issued in two K-halves, each as soon as its half of P is ready
+//   warp 2       TMEM allocator (512 columns: S_0, S_1, O_0, O_1 [, second O set when d=64])
+//   warps 4-7    norm WG 0      row r of tile 0: z += sum s^2 (packed FFMA2, registers),
+//                               P = cvt(s) -> TMEM over S, half a tile at a time
+//   warps 8-11   norm WG 1      same for tile 1, ping-ponging with WG 0
+//   warps 12-15  epilogue WG    O_t -> registers (frees TMEM for the next work tile),
+//                               O = acc * c / sqrt(c^2 z + eps) -> global
 //
 // Spherical normalisation has no exp and no running max, so O never needs
 // rescaling: it stays in TMEM for the whole K/V stream and is scaled exactly
-// once in the epilogue by c / sqrt(c^2 z + eps).  Zero padding is exact
-// (a1(0)=a2(0)=0), so ragged N uses TMA out-of-bounds zero fill, no masking.
+// once by the epilogue warpgroup, which overlaps the next work tile's MMAs.
+// Zero padding is exact (a1(0)=a2(0)=0), so ragged N uses TMA out-of-bounds
+// zero fill, no masking.
 //
 // MMA issue order per K/V tile j (keeps each norm WG a full two-MMA window):
 //     QK0(j)  PV1(j-1)  QK1(j)  PV0(j)
@@ -32,6 +38,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -40,38 +47,35 @@
 #include "../../include/flashsign.h"
 #include "sm100.cuh"
 
-#ifndef FS_VARIANT
-#define FS_VARIANT 0  // experiment knob (0 = production path)
-#endif
-#ifndef FS_TMA_ONCE
-#define FS_TMA_ONCE 0  // experiment: load the ring once, then reuse stale tiles
-#endif
-#ifndef FS_PURE_MMA
-#define FS_PURE_MMA 0  // experiment: MMA thread never waits on the norm warpgroups
-#endif
-#ifndef FS_SKIP_QK
-#define FS_SKIP_QK 0
-#endif
-#ifndef FS_SKIP_PV
-#define FS_SKIP_PV 0
-#endif
-
 namespace fs {
 
 constexpr int BM = 128;  // query rows per Q tile (= TMEM lanes)
 constexpr int BN = 128;  // keys per K/V tile
-constexpr int NQT = 2;   // Q tiles per CTA
-constexpr int NUM_THREADS = 384;
+constexpr int NQT = 2;   // Q tiles per work tile
+#ifndef FS_NWT
+#define FS_NWT 8  // norm warps per Q tile: 8 (one per lane quarter x column half) or 4
+#endif
+#ifndef FS_STAGES16
+#define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=64 16-bit, d=128 e4m3)
+#endif
+constexpr int NWT = FS_NWT;
+static_assert(NWT == 4 || NWT == 8, "norm warps per Q tile");
+constexpr int NUM_THREADS = 32 * (4 + 2 * NWT + 4);
 constexpr int TMEM_COLS = 512;
+constexpr int WARP_NORM0 = 4;              // norm warps for Q tile t = warps 4+NWT*t ..
+constexpr int WARP_EPI = 4 + 2 * NWT;      // epilogue WG = the last four warps
 
 struct KParams {
   void* o;
   int64_t o_sb, o_sn, o_sh;
   int32_t heads_q, heads_kv, seqlen_q, seqlen_kv, head_dim;
-  float g2;       // (scale * q_descale * k_descale)^2
-  float out_mul;  // scale * q_descale * k_descale * v_descale / p_scale
+  int32_t n_qblk;   // work tiles per (batch, head) = ceil(seqlen_q / (NQT*BM))
+  int32_t n_tiles;  // n_qblk * heads_q * batch
+  float g2;         // (scale * q_descale * k_descale)^2
+  float out_mul;    // scale * q_descale * k_descale * v_descale / p_scale
   float eps;
   float p_scale;
+  float ovf_z;      // (PMAX / |p_scale|)^2: a P-tile half whose sum of s^2 stays below cannot overflow
   uint64_t* bad_key;
 };
 
@@ -109,30 +113,37 @@ struct Cfg {
   static constexpr int BOXW = 128 / EB;        // elements per TMA box row
   static constexpr int Q_TILE_BYTES = BM * ROW_BYTES;
   static constexpr int SLOT_BYTES = BN * ROW_BYTES;
-  static constexpr int STAGES = (SLOT_BYTES >= 32768) ? 4 : 6;
-  static constexpr int RING_OFF = NQT * Q_TILE_BYTES;
+  // 32 KB slots (d=128, 16-bit): one Q buffer per tile, 4 ring slots.  16 KB slots (d=64 16-bit,
+  // d=128 e4m3): Q double-buffered (the next work tile's Q lands during this one), 8 ring slots.
+  static constexpr int NQB = (SLOT_BYTES >= 32768) ? 1 : 2;
+  static constexpr int STAGES = (SLOT_BYTES >= 32768) ? 4 : FS_STAGES16;
+  static constexpr int RING_OFF = NQT * NQB * Q_TILE_BYTES;
   static constexpr int BAR_OFF = RING_OFF + STAGES * SLOT_BYTES;
-  static constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
-  static constexpr int QK_STEPS = ROW_BYTES / 32;          // 32 B of K-dim per MMA
+  static constexpr int ZBUF_OFF = BAR_OFF + 512;
+  // O accumulators double-buffered in TMEM when they fit (d=64): the epilogue never gates the MMAs.
+  static constexpr int NOB = (NQT * BN + 2 * NQT * D <= TMEM_COLS) ? 2 : 1;
+  static constexpr int SMEM_BYTES = ZBUF_OFF + NQT * NOB * 2 * BM * 4 + 1024;  // + alignment slack
+  static constexpr int QK_STEPS = ROW_BYTES / 32;                          // 32 B of K-dim per MMA
   static constexpr int PV_STEPS = BN / TR::KSTEP;
-  static constexpr int P_COLS = BN * EB / 4;  // packed P columns per tile
-  static constexpr uint32_t COL_O0 = 0;
-  static constexpr uint32_t COL_S0 = NQT * D;
-  static_assert(NQT * D + NQT * BN <= TMEM_COLS, "TMEM budget");
+  static constexpr uint32_t COL_S0 = 0;
+  static constexpr uint32_t COL_O0 = NQT * BN;
+  static_assert(NQT * BN + NOB * NQT * D <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+  static_assert(PV_STEPS % 2 == 0, "PV is issued in two K-halves");
   static constexpr uint32_t IDESC_QK = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, BM, BN);
   static constexpr uint32_t IDESC_PV = ptx::idesc_make(TR::FMT, TR::FMT, 0, 1, BM, D);
 };
 
 struct Bars {
-  uint64_t q_full[NQT];
-  uint64_t kv_full[8];
-  uint64_t kv_empty[8];
+  uint64_t q_full[NQT][2], q_empty[NQT][2];
+  uint64_t kv_full[8], kv_empty[8];
   uint64_t s_full[NQT];
-  uint64_t p_full[NQT];
-  uint64_t o_full[NQT];
+  uint64_t p_full[NQT][2];  // per half of the P tile
+  uint64_t o_full[NQT][2], o_empty[NQT][2];
+  uint64_t z_full[NQT][2], z_empty[NQT][2];
   uint32_t tmem_base;
 };
+static_assert(sizeof(Bars) <= 512, "barrier block");
 
 template <int IN>
 __device__ __forceinline__ uint32_t pack2(float lo, float hi);
@@ -191,6 +202,18 @@ __device__ __forceinline__ void store32(typename OutT<OUT>::T* dst, const float*
   }
 }
 
+struct TileCoord {
+  int qblk, head, batch;
+};
+__device__ __forceinline__ TileCoord decode_tile(int tile, const KParams& p) {
+  TileCoord c;
+  c.qblk = tile % p.n_qblk;
+  const int bh = tile / p.n_qblk;
+  c.head = bh % p.heads_q;
+  c.batch = bh / p.heads_q;
+  return c;
+}
+
 template <int IN, int D, int OUT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     flashsign_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -202,23 +225,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (raw_s & 1023u)) & 1023u);
   const uint32_t smem_s = ptx::smem_u32(smem);
   Bars* bars = reinterpret_cast<Bars*>(smem + C::BAR_OFF);
+  float* zbuf = reinterpret_cast<float*>(smem + C::ZBUF_OFF);  // [NQT][NOB][2 halves][BM]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int qblk = blockIdx.x;
-  const int head = blockIdx.y;
-  const int batch = blockIdx.z;
-  const int head_kv = static_cast<int>((static_cast<int64_t>(head) * p.heads_kv) / p.heads_q);
   const int n_kv_tiles = (p.seqlen_kv + BN - 1) / BN;
-  const int q_row0 = qblk * (NQT * BM);
 
   if (threadIdx.x == 32) {
 #pragma unroll
     for (int t = 0; t < NQT; ++t) {
-      ptx::mbar_init(&bars->q_full[t], 1);
       ptx::mbar_init(&bars->s_full[t], 1);
-      ptx::mbar_init(&bars->p_full[t], 4);
-      ptx::mbar_init(&bars->o_full[t], 1);
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        ptx::mbar_init(&bars->q_full[t][b], 1);
+        ptx::mbar_init(&bars->q_empty[t][b], 1);
+        ptx::mbar_init(&bars->p_full[t][b], 4);
+        ptx::mbar_init(&bars->o_full[t][b], 1);
+        ptx::mbar_init(&bars->o_empty[t][b], 4);
+        ptx::mbar_init(&bars->z_full[t][b], NWT);
+        ptx::mbar_init(&bars->z_empty[t][b], 4);
+      }
     }
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&bars->kv_full[s], 1);
@@ -240,258 +266,303 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    if (lane == 0 && n_kv_tiles > 0) {
       const uint64_t pol_q = ptx::policy_evict_first();
       const uint64_t pol_kv = ptx::policy_evict_last();
+      uint32_t kv_i = 0;  // loads issued into the ring so far (K and V alternate)
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+        const TileCoord tc = decode_tile(tile, p);
+        const int head_kv = static_cast<int>((static_cast<int64_t>(tc.head) * p.heads_kv) / p.heads_q);
+        const int q_row0 = tc.qblk * (NQT * BM);
+        const int qb = it % C::NQB;
+        const uint32_t q_use = static_cast<uint32_t>(it / C::NQB);
 #pragma unroll
-      for (int t = 0; t < NQT; ++t) {
-        ptx::mbar_arrive_expect_tx(&bars->q_full[t], C::Q_TILE_BYTES);
+        for (int t = 0; t < NQT; ++t) {
+          ptx::mbar_wait(&bars->q_empty[t][qb], (q_use & 1u) ^ 1u);
+          ptx::mbar_arrive_expect_tx(&bars->q_full[t][qb], C::Q_TILE_BYTES);
 #pragma unroll
-        for (int db = 0; db < C::NDB; ++db)
-          ptx::tma_load_4d(smem + t * C::Q_TILE_BYTES + db * (BM * 128), &tm_q, &bars->q_full[t], db * C::BOXW,
-                           q_row0 + t * BM, head, batch, pol_q);
-      }
-      for (int i = 0; i < 2 * n_kv_tiles; ++i) {
-        const int slot = i % C::STAGES;
-        const int round = i / C::STAGES;
-        if (FS_TMA_ONCE && round > 0) break;
-        if (round > 0) ptx::mbar_wait(&bars->kv_empty[slot], (round - 1) & 1);
-        ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::SLOT_BYTES);
-        const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
-        const int key0 = (i >> 1) * BN;
+          for (int db = 0; db < C::NDB; ++db)
+            ptx::tma_load_4d(smem + (t * C::NQB + qb) * C::Q_TILE_BYTES + db * (BM * 128), &tm_q,
+                             &bars->q_full[t][qb], db * C::BOXW, q_row0 + t * BM, tc.head, tc.batch, pol_q);
+        }
+        if (C::NQB == 1 && tile + static_cast<int>(gridDim.x) < p.n_tiles) {
+          // single Q buffer: pull the next work tile's Q into L2 now so its reload is an L2 hit
+          const TileCoord nx = decode_tile(tile + gridDim.x, p);
 #pragma unroll
-        for (int db = 0; db < C::NDB; ++db)
-          ptx::tma_load_4d(smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128), tm, &bars->kv_full[slot],
-                           db * C::BOXW, key0, head_kv, batch, pol_kv);
+          for (int t = 0; t < NQT; ++t)
+#pragma unroll
+            for (int db = 0; db < C::NDB; ++db)
+              ptx::tma_prefetch_l2_4d(&tm_q, db * C::BOXW, nx.qblk * (NQT * BM) + t * BM, nx.head, nx.batch);
+        }
+        for (int i = 0; i < 2 * n_kv_tiles; ++i, ++kv_i) {
+          const uint32_t slot = kv_i % C::STAGES;
+          const uint32_t round = kv_i / C::STAGES;
+          ptx::mbar_wait(&bars->kv_empty[slot], (round & 1u) ^ 1u);
+          ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::SLOT_BYTES);
+          const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
+          const int key0 = (i >> 1) * BN;
+#pragma unroll
+          for (int db = 0; db < C::NDB; ++db)
+            ptx::tma_load_4d(smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128), tm, &bars->kv_full[slot],
+                             db * C::BOXW, key0, head_kv, tc.batch, pol_kv);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs the (warp-uniform) control flow and waits; one elected
-    // lane issues.  Descriptors are built once; per-step offsets are constants, so
-    // every MMA is a couple of uniform-register adds (~64 cycles of tensor work each).
+    // lane issues.  Descriptors are built once; per-step offsets are constants.
     if (n_kv_tiles > 0) {
       const bool leader = ptx::elect_one();
       const uint64_t q_desc = ptx::sdesc_sw128(smem_s, 16, 1024);
       const uint64_t k_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, 16, 1024);
       const uint64_t v_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, BN * 128, 1024);
-      auto qk = [&](int t, int slot) {
-        if (FS_SKIP_QK) return;
-        const uint64_t a0 = q_desc + static_cast<uint32_t>((t * C::Q_TILE_BYTES) >> 4);
-        const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
-        const uint32_t d_tmem = tmem + C::COL_S0 + t * BN;
+      uint32_t kv_i = 0;                 // ring position of this work tile's K_0
+      uint32_t p_use[NQT] = {0u, 0u};    // completed phases of p_full[t][*]
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+        const int qb = it % C::NQB;
+        const uint32_t q_use = static_cast<uint32_t>(it / C::NQB);
+        const int ob = it % C::NOB;
+        const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
+        auto qk = [&](int t, uint32_t slot) {
+          const uint64_t a0 = q_desc + static_cast<uint32_t>(((t * C::NQB + qb) * C::Q_TILE_BYTES) >> 4);
+          const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
+          const uint32_t d_tmem = tmem + C::COL_S0 + t * BN;
 #pragma unroll
-        for (int ks = 0; ks < C::QK_STEPS; ++ks) {
-          const uint32_t off_a = ((ks * 32 / 128) * (BM * 128) + (ks * 32) % 128) >> 4;
-          const uint32_t off_b = ((ks * 32 / 128) * (BN * 128) + (ks * 32) % 128) >> 4;
-          if constexpr (TR::F8)
-            ptx::mma_f8_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
-          else
-            ptx::mma_f16_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
-        }
-      };
-      auto pv = [&](int t, int slot, bool acc) {
-        if (FS_SKIP_PV) return;
-        const uint64_t b0 = v_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
-        const uint32_t a_tmem = tmem + C::COL_S0 + t * BN;
-        const uint32_t d_tmem = tmem + C::COL_O0 + t * D;
+          for (int ks = 0; ks < C::QK_STEPS; ++ks) {
+            const uint32_t off_a = ((ks * 32 / 128) * (BM * 128) + (ks * 32) % 128) >> 4;
+            const uint32_t off_b = ((ks * 32 / 128) * (BN * 128) + (ks * 32) % 128) >> 4;
+            if constexpr (TR::F8)
+              ptx::mma_f8_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
+            else
+              ptx::mma_f16_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
+          }
+        };
+        // O_t += P_t V_j, one K-half at a time as the norm WG finishes that half of P
+        auto pv = [&](int t, uint32_t slot, int j) {
+          if (j == 0) ptx::mbar_wait(&bars->o_empty[t][ob], (o_use & 1u) ^ 1u);
+          const uint64_t b0 = v_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
+          const uint32_t a_tmem = tmem + C::COL_S0 + t * BN;
+          const uint32_t d_tmem = tmem + C::COL_O0 + (ob * NQT + t) * D;
 #pragma unroll
-        for (int ks = 0; ks < C::PV_STEPS; ++ks) {
-          const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
-          const uint32_t at = a_tmem + ks * (TR::KSTEP * C::EB / 4);
-          if constexpr (TR::F8)
-            ptx::mma_f8_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, (acc || ks > 0) ? 1u : 0u);
-          else
-            ptx::mma_f16_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, (acc || ks > 0) ? 1u : 0u);
-        }
-      };
+          for (int h = 0; h < 2; ++h) {
+            ptx::mbar_wait(&bars->p_full[t][h], p_use[t] & 1u);
+            ptx::tc_fence_after();
+            if (leader) {
 #pragma unroll
-      for (int t = 0; t < NQT; ++t) ptx::mbar_wait(&bars->q_full[t], 0);
-      ptx::tc_fence_after();
-      // ring position of K_j (even loads) and V_j (odd loads)
-      int k_slot = 0, k_phase = 0;
-      int v_slot = 1 % C::STAGES, v_phase = (1 >= C::STAGES) ? 1 : 0;
-      int prev_v_slot = 0;
-      for (int j = 0; j < n_kv_tiles; ++j) {
-        if (!FS_TMA_ONCE || 2 * j < C::STAGES) ptx::mbar_wait(&bars->kv_full[k_slot], k_phase);
+              for (int k2 = 0; k2 < C::PV_STEPS / 2; ++k2) {
+                const int ks = h * (C::PV_STEPS / 2) + k2;
+                const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
+                const uint32_t at = a_tmem + h * (BN / 2) + k2 * (TR::KSTEP * C::EB / 4);
+                const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
+                if constexpr (TR::F8)
+                  ptx::mma_f8_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
+                else
+                  ptx::mma_f16_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
+              }
+            }
+            __syncwarp();
+          }
+          ++p_use[t];
+        };
+#pragma unroll
+        for (int t = 0; t < NQT; ++t) ptx::mbar_wait(&bars->q_full[t][qb], q_use & 1u);
         ptx::tc_fence_after();
-        if (leader) {
-          qk(0, k_slot);
-          ptx::tc_commit(&bars->s_full[0]);
-        }
-        __syncwarp();
-        if (j > 0) {
-          if (!FS_PURE_MMA) ptx::mbar_wait(&bars->p_full[1], (j - 1) & 1);
+        uint32_t prev_v_slot = 0;
+        for (int j = 0; j < n_kv_tiles; ++j) {
+          const uint32_t k_idx = kv_i + 2 * j, v_idx = k_idx + 1;
+          const uint32_t k_slot = k_idx % C::STAGES, v_slot = v_idx % C::STAGES;
+          ptx::mbar_wait(&bars->kv_full[k_slot], (k_idx / C::STAGES) & 1u);
           ptx::tc_fence_after();
           if (leader) {
-            pv(1, prev_v_slot, j - 1 > 0);
-            ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
+            qk(0, k_slot);
+            ptx::tc_commit(&bars->s_full[0]);
+            if (j == n_kv_tiles - 1) ptx::tc_commit(&bars->q_empty[0][qb]);
           }
           __syncwarp();
+          if (j > 0) {
+            pv(1, prev_v_slot, j - 1);
+            if (leader) ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
+            __syncwarp();
+          }
+          if (leader) {
+            qk(1, k_slot);
+            ptx::tc_commit(&bars->s_full[1]);
+            ptx::tc_commit(&bars->kv_empty[k_slot]);
+            if (j == n_kv_tiles - 1) ptx::tc_commit(&bars->q_empty[1][qb]);
+          }
+          __syncwarp();
+          ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
+          pv(0, v_slot, j);
+          if (j == n_kv_tiles - 1) {
+            if (leader) ptx::tc_commit(&bars->o_full[0][ob]);
+            __syncwarp();
+          }
+          prev_v_slot = v_slot;
         }
+        pv(1, prev_v_slot, n_kv_tiles - 1);
         if (leader) {
-          qk(1, k_slot);
-          ptx::tc_commit(&bars->s_full[1]);
-          ptx::tc_commit(&bars->kv_empty[k_slot]);
+          ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
+          ptx::tc_commit(&bars->o_full[1][ob]);
         }
         __syncwarp();
-        if (!FS_TMA_ONCE || 2 * j + 1 < C::STAGES) ptx::mbar_wait(&bars->kv_full[v_slot], v_phase);
-        if (!FS_PURE_MMA) ptx::mbar_wait(&bars->p_full[0], j & 1);
-        ptx::tc_fence_after();
-        if (leader) {
-          pv(0, v_slot, j > 0);
-          if (j == n_kv_tiles - 1) ptx::tc_commit(&bars->o_full[0]);
-        }
-        __syncwarp();
-        prev_v_slot = v_slot;
-        // advance both ring cursors by two loads
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          if (++k_slot == C::STAGES) { k_slot = 0; k_phase ^= 1; }
-          if (++v_slot == C::STAGES) { v_slot = 0; v_phase ^= 1; }
-        }
+        kv_i += 2 * n_kv_tiles;
       }
-      if (!FS_PURE_MMA) ptx::mbar_wait(&bars->p_full[1], (n_kv_tiles - 1) & 1);
-      ptx::tc_fence_after();
-      if (leader) {
-        pv(1, prev_v_slot, n_kv_tiles - 1 > 0);
-        ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
-        ptx::tc_commit(&bars->o_full[1]);
-      }
-      __syncwarp();
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ norm warpgroups
-    const int t = (warp - 4) >> 2;  // Q tile owned by this warpgroup
-    const int quarter = warp & 3;   // TMEM lane quarter this warp may access
+  } else if (warp >= WARP_NORM0 && warp < WARP_EPI) {
+    // ------------------------------------------------------------ norm warps
+    // Eight warps per Q tile: warp (t, h, quarter) owns TMEM lanes 32*quarter.. and the
+    // score columns [64h, 64h+64) of S_t, so both halves of P are produced in parallel.
+    // P half h is packed into the first columns of its own S half (never over unread S).
+    // (With NWT=4 a warp owns all 128 columns and produces the two halves in turn.)
+    const int t = (warp - WARP_NORM0) / NWT;                             // Q tile
+    const int hh0 = NWT == 8 ? ((warp - WARP_NORM0) >> 2) & 1 : 0;      // first column half
+    constexpr int NH = NWT == 8 ? 1 : 2;                                 // halves per warp
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t s_addr = tmem + lane_off + C::COL_S0 + t * BN;
-    const uint32_t o_addr = tmem + lane_off + C::COL_O0 + t * D;
+    const uint32_t s_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + C::COL_S0 + t * BN;
     const float ps = p.p_scale;
-    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-    float amax = 0.f;
-    for (int j = 0; j < (FS_PURE_MMA ? 0 : n_kv_tiles); ++j) {
-      ptx::mbar_wait(&bars->s_full[t], j & 1);
-      ptx::tc_fence_after();
-#if FS_VARIANT == 3
-      // experiment: no TMEM traffic at all
-#elif FS_VARIANT == 5
-      {
-        uint32_t s[128];
-        ptx::tmem_ld32(s_addr + 0, s);
-        ptx::tmem_ld32(s_addr + 32, s + 32);
-        ptx::tmem_ld32(s_addr + 64, s + 64);
-        ptx::tmem_ld32(s_addr + 96, s + 96);
+    uint32_t s_use = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles && n_kv_tiles > 0; tile += gridDim.x, ++it) {
+      const int ob = it % C::NOB;
+      float2 za = make_float2(0.f, 0.f), zb = za;
+      bool ovf = false;
+      for (int j = 0; j < n_kv_tiles; ++j) {
+        ptx::mbar_wait(&bars->s_full[t], s_use & 1u);
+        ++s_use;
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int hi = 0; hi < NH; ++hi) {
+        const int hh = hh0 + hi;
+        const uint32_t s_addr = s_base + hh * (BN / 2);
+        // 64 columns in two 32-column chunks (80 registers/thread at 768 threads): chunk 1's TMEM
+        // load is issued once chunk 0 is packed, and overlaps chunk 0's P store.
+        uint32_t s[32];
+        ptx::tmem_ld32(s_addr, s);
         ptx::tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 128; i += 4) {
-          const float a = __uint_as_float(s[i]), b = __uint_as_float(s[i + 1]);
-          const float c = __uint_as_float(s[i + 2]), d = __uint_as_float(s[i + 3]);
-          z0 = fmaf(a, a, z0);
-          z1 = fmaf(b, b, z1);
-          z2 = fmaf(c, c, z2);
-          z3 = fmaf(d, d, z3);
-        }
-        if constexpr (!TR::F8) {
+        for (int ch = 0; ch < 2; ++ch) {
+          // sum of squares: packed FP32 FMAs, two independent chains
+          float2 h0 = make_float2(0.f, 0.f), h1 = h0;
 #pragma unroll
-          for (int i = 0; i < 64; ++i) s[i] = pack2<IN>(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
-          ptx::tmem_st32(s_addr, s);
-          ptx::tmem_st32(s_addr + 32, s + 32);
-        }
-      }
-#else
+          for (int i = 0; i < 32; i += 4) {
+            const float2 a = make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1]));
+            const float2 b = make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+            h0 = __ffma2_rn(a, a, h0);
+            h1 = __ffma2_rn(b, b, h1);
+          }
+          za = __fadd2_rn(za, h0);
+          zb = __fadd2_rn(zb, h1);
+          if constexpr (TR::CHECK_OVF) {
+            // max|s| <= sqrt(sum s^2): only a chunk whose sum reaches (PMAX/|ps|)^2 can overflow P
+            const float zh = (h0.x + h0.y) + (h1.x + h1.y);
+            if (zh >= p.ovf_z) {
+              float amax = 0.f;
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t s[64];
-#if FS_VARIANT == 1
-#pragma unroll
-        for (int i = 0; i < 64; ++i) s[i] = __float_as_uint((float)(lane + i));
-#else
-        ptx::tmem_ld32(s_addr + half * 64, s);
-        ptx::tmem_ld32(s_addr + half * 64 + 32, s + 32);
-        ptx::tmem_wait_ld();
-#endif
-#if FS_VARIANT != 2
-#pragma unroll
-        for (int i = 0; i < 64; i += 4) {
-          const float a = __uint_as_float(s[i]), b = __uint_as_float(s[i + 1]);
-          const float c = __uint_as_float(s[i + 2]), d = __uint_as_float(s[i + 3]);
-          z0 = fmaf(a, a, z0);
-          z1 = fmaf(b, b, z1);
-          z2 = fmaf(c, c, z2);
-          z3 = fmaf(d, d, z3);
-          if constexpr (TR::CHECK_OVF) amax = fmaxf(amax, fmaxf(fmaxf(fabsf(a), fabsf(b)), fmaxf(fabsf(c), fabsf(d))));
-        }
-        if constexpr (TR::F8) {
+              for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(__uint_as_float(s[i])));
+              if (amax * fabsf(ps) > TR::PMAX) ovf = true;
+            }
+          }
+          // pack P (s[i] is written only after s[2i], s[2i+1] / s[4i..4i+3] are read)
           uint32_t pk[16];
+          if constexpr (TR::F8) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            pk[i] = pack4_e4m3(ps * __uint_as_float(s[4 * i]), ps * __uint_as_float(s[4 * i + 1]),
-                               ps * __uint_as_float(s[4 * i + 2]), ps * __uint_as_float(s[4 * i + 3]));
-          ptx::tmem_st16(s_addr + half * 16, pk);
-        } else {
-          uint32_t pk[32];
-          if (ps == 1.0f) {
+            for (int i = 0; i < 8; ++i)
+              pk[i] = pack4_e4m3(ps * __uint_as_float(s[4 * i]), ps * __uint_as_float(s[4 * i + 1]),
+                                 ps * __uint_as_float(s[4 * i + 2]), ps * __uint_as_float(s[4 * i + 3]));
+          } else if (ps == 1.0f) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) pk[i] = pack2<IN>(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
+            for (int i = 0; i < 16; ++i) pk[i] = pack2<IN>(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
+            for (int i = 0; i < 16; ++i)
               pk[i] = pack2<IN>(ps * __uint_as_float(s[2 * i]), ps * __uint_as_float(s[2 * i + 1]));
           }
-          ptx::tmem_st32(s_addr + half * 32, pk);
+          if (ch == 0) ptx::tmem_ld32(s_addr + 32, s);  // chunk 1 (reuses s: chunk 0 is consumed)
+          if constexpr (TR::F8)
+            ptx::tmem_st8(s_addr + ch * 8, pk);
+          else
+            ptx::tmem_st16(s_addr + ch * 16, pk);
+          if (ch == 0) ptx::tmem_wait_ld();
         }
-#else
-        z0 += __uint_as_float(s[half]);
-#endif
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&bars->p_full[t][hh]);
+        }
       }
-#endif
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
+      // hand this half's z to the epilogue warpgroup and move on to the next work tile
+      const float z = (za.x + za.y) + (zb.x + zb.y);
+      ptx::mbar_wait(&bars->z_empty[t][ob], (static_cast<uint32_t>(it / C::NOB) & 1u) ^ 1u);
+      zbuf[((t * C::NOB + ob) * 2 + hh0) * BM + r] = ovf ? __int_as_float(0x7f800000) : z;
+      if (NWT == 4) zbuf[((t * C::NOB + ob) * 2 + 1) * BM + r] = 0.f;
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->p_full[t]);
+      if (lane == 0) ptx::mbar_arrive(&bars->z_full[t][ob]);
     }
-    // ------------------------------------------------------------ epilogue
-    const float z = (z0 + z1) + (z2 + z3);
-    const float zr = p.g2 * z;  // = sum_j (c s_ij)^2, what the reference calls z
-    const float den = sqrtf(zr + p.eps);
-    bool bad = !(den > 0.f) || isinf(den);
-    float z_report = zr;
-    if constexpr (TR::CHECK_OVF) {
-      if (amax * fabsf(ps) > TR::PMAX) {
-        bad = true;
-        z_report = __int_as_float(0x7f800000);
-      }
-    }
-    const int row = q_row0 + t * BM + r;
-    if (n_kv_tiles > 0) {
-      ptx::mbar_wait(&bars->o_full[t], 0);
-      ptx::tc_fence_after();
-    }
+  } else if (warp >= WARP_EPI) {
+    // ------------------------------------------------------------ epilogue warpgroup
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     using OT = typename OutT<OUT>::T;
-    OT* dst = reinterpret_cast<OT*>(p.o) + batch * p.o_sb + static_cast<int64_t>(row) * p.o_sn + head * p.o_sh;
-    const bool live = row < p.seqlen_q;
-    if (live && bad && p.bad_key != nullptr) {
-      const uint64_t lin = (static_cast<uint64_t>(batch) * p.heads_q + head) * p.seqlen_q + row;
-      atomicMin(reinterpret_cast<unsigned long long*>(p.bad_key),
-                static_cast<unsigned long long>((lin << 32) | __float_as_uint(z_report)));
-    }
-    const float mul = p.out_mul;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+      const TileCoord tc = decode_tile(tile, p);
+      const int ob = it % C::NOB;
+      const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t acc[32];
-      float v[32];
-      ptx::tmem_ld32(o_addr + c * 32, acc);  // warp-collective: every lane participates
-      ptx::tmem_wait_ld();
-      if (n_kv_tiles == 0) {
+      for (int t = 0; t < NQT; ++t) {
+        // zr = sum_j (c s_ij)^2 (what the reference calls z), or +inf for a P overflow
+        float zr = 0.f;
+        if (n_kv_tiles > 0) {
+          ptx::mbar_wait(&bars->z_full[t][ob], o_use & 1u);
+          const float* zt = zbuf + (t * C::NOB + ob) * 2 * BM + r;
+          zr = p.g2 * (zt[0] + zt[BM]);  // the two column halves of the row
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&bars->z_empty[t][ob]);
+        }
+        const float den = sqrtf(zr + p.eps);
+        const bool bad = !(den > 0.f) || isinf(den);
+        const float mul = __fdiv_rn(p.out_mul, den);
+        const int row = tc.qblk * (NQT * BM) + t * BM + r;
+        const bool live = row < p.seqlen_q;
+        if (live && bad && p.bad_key != nullptr) {
+          const uint64_t lin = (static_cast<uint64_t>(tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
+          atomicMin(reinterpret_cast<unsigned long long*>(p.bad_key),
+                    static_cast<unsigned long long>((lin << 32) | __float_as_uint(zr)));
+        }
+        OT* dst = reinterpret_cast<OT*>(p.o) + tc.batch * p.o_sb + static_cast<int64_t>(row) * p.o_sn +
+                  tc.head * p.o_sh;
+        const uint32_t o_addr = tmem + lane_off + C::COL_O0 + (ob * NQT + t) * D;
+        if (n_kv_tiles > 0) {
+          ptx::mbar_wait(&bars->o_full[t][ob], o_use & 1u);
+          ptx::tc_fence_after();
+        }
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t acc[32];
+          float v[32];
+          if (n_kv_tiles > 0) {
+            ptx::tmem_ld32(o_addr + c * 32, acc);  // warp-collective: every lane participates
+            ptx::tmem_wait_ld();
+            if (c == D / 32 - 1) {  // all of O_t is in registers: release the accumulator
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(&bars->o_empty[t][ob]);
+            }
+          } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] = 0u;
+            for (int i = 0; i < 32; ++i) acc[i] = 0u;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(acc[i]) * mul;
+          if (live && c * 32 < p.head_dim) store32<OUT>(dst + c * 32, v, c * 32, p.head_dim);
+        }
       }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __fdiv_rn(mul * __uint_as_float(acc[i]), den);
-      if (live && c * 32 < p.head_dim) store32<OUT>(dst + c * 32, v, c * 32, p.head_dim);
     }
   }
 
@@ -547,6 +618,23 @@ static bool encode_bshd(CUtensorMap* map, CUtensorMapDataType dt, int eb, const 
   return true;
 }
 
+// SM count of the current device (persistent grid size), cached per device.
+static int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (dev < 0 || dev >= 64) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) cache[dev] = n;
+  }
+  return cache[dev];
+}
+
 template <int IN, int D, int OUT>
 static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   using C = Cfg<IN, D>;
@@ -587,8 +675,15 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   kp.eps = p->eps;
   kp.p_scale = p->p_scale;
   kp.bad_key = p->bad_key;
-
-  dim3 grid((p->seqlen_q + NQT * BM - 1) / (NQT * BM), p->heads_q, p->batch);
+  const double pmax = InTraits<IN>::PMAX / std::fabs((double)p->p_scale);
+  kp.ovf_z = (float)std::fmin(pmax * pmax, 3.0e38);
+  const int64_t n_qblk = (p->seqlen_q + NQT * BM - 1) / (NQT * BM);
+  const int64_t n_tiles = n_qblk * p->heads_q * p->batch;
+  if (n_tiles > INT32_MAX) return fail(FS_ERR_UNSUPPORTED, "too many work tiles for one launch");
+  kp.n_qblk = (int32_t)n_qblk;
+  kp.n_tiles = (int32_t)n_tiles;
+  const int grid = (int)std::min<int64_t>(n_tiles, num_sms());
+  if (grid <= 0) return fail(FS_ERR_CUDA, "no SMs reported for the current device");
   kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, kp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));

@@ -41,6 +41,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Warpgroup register rebalancing (all four warps of a warpgroup execute the same one).
+template <uint32_t N>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -84,11 +94,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint64_t t0 = globaltimer();
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
-    if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 4000000000ull) {
-      printf("flashsign watchdog: block (%d,%d,%d) thread %d stuck on mbarrier %u parity %u\n",
-             blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, a, parity);
-      __trap();
-    }
+    // no printf here: a call would make every waiting role spill its live registers
+    if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
   }
 }
 
@@ -105,6 +112,14 @@ __device__ __forceinline__ void tma_load_4d(void* smem_dst, const void* tmap, ui
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
       "l"(cache_policy)
       : "memory");
+}
+
+// Pull a tile into L2 ahead of its real load (no shared-memory destination, no barrier).
+__device__ __forceinline__ void tma_prefetch_l2_4d(const void* tmap, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -1,0 +1,139 @@
+"""A/B timing of kernel build variants in one process (experiment tool, not a test).
+
+    python tests/ab_variants.py build base= nwt4=-DFS_NWT=4      # here (nvcc cross-compiles)
+    python tests/ab_variants.py run [c2 c3 c4 c5] [--rounds R]   # on the GPU box
+
+``build`` compiles csrc/flashsign_fwd.cu once per NAME=FLAGS into
+paper_2505_09326_b200/_lib/ab/libfs_NAME.so.  ``run`` loads every variant and, per
+configuration, alternates them round-robin (same thermal/power state), timing
+back-to-back launches with CUDA events while NVML samples the SM clock.  Reports the
+median TFLOP/s, the median SM clock and TFLOP/s per GHz -> gpurun_out/ab_variants.json.
+"""
+
+import ctypes
+import glob
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+AB_DIR = os.path.join(ROOT, "paper_2505_09326_b200", "_lib", "ab")
+
+CASES = {  # name: (B, N, H, D, dtype, eps)
+    "c2": (16, 4096, 16, 64, "fp16", 0.0),
+    "c3": (8, 16384, 16, 128, "bf16", 0.0),
+    "c4": (8, 8192, 16, 128, "e4m3", 0.0),
+    "c5": (64, 20000, 8, 64, "bf16", 1e-6),
+}
+
+
+def build(specs):
+    from paper_2505_09326_b200 import build as b
+    os.makedirs(AB_DIR, exist_ok=True)
+    for spec in specs:
+        name, _, flags = spec.partition("=")
+        out = os.path.join(AB_DIR, f"libfs_{name}.so")
+        cmd = [b._nvcc(), *b.NVCC_FLAGS, *flags.split(), "-o", out, os.path.join(b.CSRC, "flashsign_fwd.cu")]
+        print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True, cwd=b.CSRC)
+
+
+def run(cases, rounds):
+    import torch
+    from paper_2505_09326_b200 import _lib
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    except Exception:
+        pynvml = None
+    libs = {}
+    for path in sorted(glob.glob(os.path.join(AB_DIR, "libfs_*.so"))):
+        lib = ctypes.CDLL(path)
+        lib.fs_fwd.argtypes = [ctypes.POINTER(_lib.FsFwdParams), ctypes.c_void_p]
+        lib.fs_fwd.restype = ctypes.c_int
+        lib.fs_last_error.restype = ctypes.c_char_p
+        libs[os.path.basename(path)[6:-3]] = lib
+    tdt = {"fp16": torch.float16, "bf16": torch.bfloat16, "e4m3": torch.float8_e4m3fn}
+    code = {"fp16": _lib.FS_F16, "bf16": _lib.FS_BF16, "e4m3": _lib.FS_E4M3}
+    res = {}
+    for cname in cases:
+        B, N, H, D, dt, eps = CASES[cname]
+        g = torch.Generator(device="cuda").manual_seed(0)
+        q, k, v = (torch.randn((B, N, H, D), generator=g, device="cuda").to(tdt[dt]) for _ in range(3))
+        odt = torch.float16 if dt == "fp16" else torch.bfloat16
+        o = torch.empty((B, N, H, D), dtype=odt, device="cuda")
+        bad = torch.empty(1, dtype=torch.int64, device="cuda")
+        p = _lib.FsFwdParams()
+        p.q, p.k, p.v, p.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr()
+        for dst, t in ((p.q_stride, q), (p.k_stride, k), (p.v_stride, v), (p.o_stride, o)):
+            dst[0], dst[1], dst[2] = t.stride(0), t.stride(1), t.stride(2)
+        p.batch, p.heads_q, p.heads_kv, p.seqlen_q, p.seqlen_kv, p.head_dim = B, H, H, N, N, D
+        p.in_dtype, p.out_dtype = code[dt], (_lib.FS_F16 if dt == "fp16" else _lib.FS_BF16)
+        p.scale, p.eps, p.p_scale, p.q_descale, p.k_descale, p.v_descale = 1.0, eps, 1.0, 1.0, 1.0, 1.0
+        p.bad_key = bad.data_ptr()
+        flops = 4.0 * B * H * N * N * D
+        s = torch.cuda.current_stream().cuda_stream
+        est_ms = flops / 1.2e15 * 1e3
+        n = max(5, int(300.0 / est_ms))  # ~300 ms of back-to-back launches per sample
+        samples = {name: [] for name in libs}
+        outs = {}
+        for rnd in range(rounds + 1):
+            for name, lib in libs.items():
+                for _ in range(2):
+                    rc = lib.fs_fwd(ctypes.byref(p), ctypes.c_void_p(s))
+                    assert rc == 0, lib.fs_last_error()
+                torch.cuda.synchronize()
+                clk, stop = [], threading.Event()
+
+                def sampler():
+                    while not stop.is_set():
+                        if pynvml is not None:
+                            clk.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        time.sleep(0.01)
+                th = threading.Thread(target=sampler, daemon=True)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                th.start()
+                e0.record()
+                for _ in range(n):
+                    lib.fs_fwd(ctypes.byref(p), ctypes.c_void_p(s))
+                e1.record()
+                torch.cuda.synchronize()
+                stop.set()
+                th.join()
+                ms = e0.elapsed_time(e1) / n
+                mhz = statistics.median(clk) if clk else float("nan")
+                if rnd > 0:  # round 0 is a warm-up
+                    samples[name].append((flops / ms / 1e9, mhz))
+                if rnd == 1:
+                    outs[name] = o.float().clone()
+        ref = next(iter(outs.values()))
+        for name in libs:
+            tf = statistics.median(x[0] for x in samples[name])
+            mhz = statistics.median(x[1] for x in samples[name])
+            diff = float((outs[name] - ref).abs().max())
+            res[f"{cname}/{name}"] = {"tflops": round(tf, 1), "sm_mhz": mhz, "tflops_per_ghz": round(tf / mhz * 1e3, 1),
+                                      "max_abs_vs_first": diff, "launches_per_sample": n}
+            print(cname, name, res[f"{cname}/{name}"], flush=True)
+        del q, k, v, o
+        torch.cuda.empty_cache()
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "ab_variants.json"), "w") as f:
+        json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build(sys.argv[2:])
+    else:
+        args = [a for a in sys.argv[2:] if not a.startswith("--")]
+        rounds = 3
+        if "--rounds" in sys.argv:
+            rounds = int(sys.argv[sys.argv.index("--rounds") + 1])
+            args = [a for a in args if a != str(rounds)]
+        run(args or list(CASES), rounds)
