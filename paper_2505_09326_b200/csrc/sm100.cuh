@@ -85,6 +85,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity
   return ok != 0;
 }
 
+// try_wait with an explicit suspend-time limit (ns): the warp sleeps in hardware until the
+// phase completes or the limit expires, instead of re-issuing the probe.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar_addr, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar_addr), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+
+#ifndef FS_WAIT_HINT
+#define FS_WAIT_HINT 0  // 0: system-default try_wait time limit
+#endif
+
 // Blocking wait on the phase with the given parity.  A watchdog turns a
 // protocol bug into a trapped launch (cudaErrorLaunchFailure) after ~4 s
 // instead of a hung GPU.
@@ -93,7 +111,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(a, parity)) return;
   const uint64_t t0 = globaltimer();
   uint32_t spins = 0;
-  while (!mbar_try_wait(a, parity)) {
+  while (!(FS_WAIT_HINT ? mbar_try_wait_hint(a, parity, FS_WAIT_HINT) : mbar_try_wait(a, parity))) {
     // no printf here: a call would make every waiting role spill its live registers
     if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
   }

@@ -112,6 +112,22 @@ def run(cases, rounds):
                     samples[name].append((flops / ms / 1e9, mhz))
                 if rnd == 1:
                     outs[name] = o.float().clone()
+        for name, lib in libs.items():  # diagnostic builds (-DFS_PROF=1): per-event latencies, one launch
+            if not hasattr(lib, "fs_prof_read"):
+                continue
+            buf = (ctypes.c_ulonglong * 16)()
+            lib.fs_prof_read(buf)
+            lib.fs_fwd(ctypes.byref(p), ctypes.c_void_p(s))
+            torch.cuda.synchronize()
+            lib.fs_prof_read(buf)
+            b = list(buf)
+            prof = {"norm_cyc_per_tile": b[0] / max(b[1], 1), "norm_wait_s_cyc": b[6] / max(b[1], 1),
+                    "mma_wait_p_cyc": b[2] / max(b[3], 1), "mma_wait_kv_cyc": b[4] / max(b[5], 1),
+                    "mma_cyc_per_kv_tile": b[7] / max(b[5], 1), "mma_wait_v_per_kv": b[8] / max(b[5], 1),
+                    "mma_wait_o_per_kv": b[9] / max(b[5], 1), "mma_wait_q_per_kv": b[10] / max(b[5], 1),
+                    "mma_qk_issue_per_kv": b[11] / max(b[5], 1)}
+            res[f"{cname}/{name}/prof"] = prof
+            print(cname, name, "prof", {k: round(v, 1) for k, v in prof.items()}, flush=True)
         ref = next(iter(outs.values()))
         for name in libs:
             tf = statistics.median(x[0] for x in samples[name])

@@ -13,6 +13,8 @@ using namespace fs::ptx;
 // MODE 1: SS  M128 N256
 // MODE 2: TS  M128 N128 (A tmem, B MN-major)   -- PV
 // MODE 3: alternating groups MODE0 / MODE2     -- QK, PV interleaved, like FlashSign
+// MODE 4: d=64 pattern: 4 SS M128N128 (QK, K=64) then 8 TS M128N64 (PV, 128 keys) per group
+// MODE 5: 8 TS M128N64 only
 template <int MODE, bool WARP, bool COMMIT, int NACC>
 __global__ void __launch_bounds__(128, 1) mma_bench(int n_groups, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -39,6 +41,22 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int n_groups, unsigned long 
       const bool leader = WARP ? elect_one() : true;
       const uint32_t acc = (NACC == 1) ? 0u : (uint32_t)(g & 1) * 128u;
       const bool do_pv = (MODE == 2) || (MODE == 3 && (g & 1));
+      if (MODE >= 4) {
+        if (leader) {
+          constexpr uint32_t id_qk64 = idesc_make(1, 1, 0, 0, 128, 128);
+          constexpr uint32_t id_pv64 = idesc_make(1, 1, 0, 1, 128, 64);
+          if (MODE == 4) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) mma_f16_ss(tmem + acc, da + ks * 2, db + ks * 2, id_qk64, ks > 0);
+          }
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            mma_f16_ts(tmem + 256 + (acc % 256) / 2, tmem + 448 + ks * 8, dv + ((ks * 2048) >> 4), id_pv64, ks > 0);
+          if (COMMIT) tc_commit(&bar2);
+        }
+        if (WARP) __syncwarp();
+        continue;
+      }
       if (leader) {
         if (!do_pv) {
 #pragma unroll
@@ -91,5 +109,6 @@ extern "C" int run_mma_bench(int mode, int warp_issue, int commit, int nacc, int
   CASE(1, 1, 0, 1) CASE(1, 1, 1, 1)
   CASE(2, 0, 0, 1) CASE(2, 1, 0, 1) CASE(2, 1, 1, 1) CASE(2, 1, 1, 2)
   CASE(3, 1, 0, 2) CASE(3, 1, 1, 2) CASE(3, 0, 1, 2)
+  CASE(4, 1, 0, 2) CASE(4, 1, 1, 2) CASE(5, 1, 0, 1) CASE(5, 1, 1, 2)
   return 2;
 }

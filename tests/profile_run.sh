@@ -16,7 +16,9 @@ for c in c3 c2 c4 c5; do
     --clock-control none -k regex:flashsign -c 3 --csv --log-file $OUT/launches_$c.csv \
     python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:flashsign -s 3 -c 1 -o $OUT/prof_c3 \
-  python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_c3.log 2>&1
+for c in c3 c2; do
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:flashsign -s 3 -c 1 -o $OUT/prof_$c \
+  python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_$c.log 2>&1
+done
 tail -2 $OUT/ncu_c3.log
 ls -la $OUT
