@@ -36,8 +36,8 @@ CONFIGS = {
     "c2": dict(B=16, H=16, HKV=16, N=4096, D=64, dtype="fp16", eps=0.0, desc="B16 H16 N4096 d64 fp16"),
     "c3": dict(B=8, H=16, HKV=16, N=16384, D=128, dtype="bf16", eps=0.0, desc="B8 H16 N16384 d128 bf16"),
     "c4": dict(B=8, H=16, HKV=16, N=8192, D=128, dtype="e4m3", eps=0.0, desc="B8 H16 N8192 d128 e4m3 (bf16 out)"),
-    "c5": dict(B=64, H=8, HKV=8, N=20000, D=64, dtype="bf16", eps=1e-6,
-               desc="GRN B64 H8 N20000 d64 bf16, eps=1e-6, multiplicity-scaled K"),
+    "c5": dict(B=64, H=8, HKV=8, N=20000, D=64, dtype="bf16", eps=1e-6, mult=True,
+               desc="GRN B64 H8 N20000 d64 bf16, eps=1e-6, multiplicity-scaled keys m in {0..5}"),
 }
 PAPER_A100_TFLOPS = 200.0  # PAPER.md:199 (FlashSign fwd, d=128, FP16, A100) -- BASELINE.md section 1
 
@@ -49,6 +49,29 @@ def load_peaks():
         return p, "measured"
     except Exception:
         return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def measure_fp8_peak(device, n: int = 8192, reps: int = 10):
+    """Dense e4m3 tensor-core roofline measured in this run: cuBLASLt
+    ``torch._scaled_mm`` n^3, best of ``reps`` (burst, like MEASURED_PEAKS' bf16 figure)."""
+    import torch
+    try:
+        a = torch.randn((n, n), device=device).to(torch.float8_e4m3fn)
+        b = torch.randn((n, n), device=device).to(torch.float8_e4m3fn).t()
+        one = torch.ones((), device=device)
+        torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -109,7 +132,8 @@ def make_inputs(cfg, lo, hi, device, seed=1000):
 
     Deterministic per unit: unit u's Q/K/V come from a generator seeded with
     seed+u, so a shard's data equals the same units of a 1-GPU run.
-    Returns q, k, v for batch rows [b_lo, b_hi) and the unit offset.
+    Returns q, k, v for batch rows [b_lo, b_hi), the per-key multiplicities m
+    [rows, N] (GRN configuration, else None) and the unit offset.
     """
     import torch
     B, H, HKV, N, D = cfg["B"], cfg["H"], cfg["HKV"], cfg["N"], cfg["D"]
@@ -121,18 +145,26 @@ def make_inputs(cfg, lo, hi, device, seed=1000):
     k = torch.empty((nb, N, HKV, D), dtype=tdt, device=device)
     v = torch.empty((nb, N, HKV, D), dtype=tdt, device=device)
     g = torch.Generator(device=device)
+    # GRN: one multiplicity per gene (key) and cell (batch row), m in {0..5} (cli.py:296; grn.py:150).
+    # Default: the caller's K' = m K (attention.py:381-388) is applied here, outside the timed region,
+    # as the reference's grn._layer_qkv does before calling attention.  --fused-mult instead passes m
+    # to the kernel (key_scale), which scales each score in fp32.
+    m = torch.empty((nb, N), dtype=torch.float32, device=device) if cfg.get("mult") else None
     for u in range(max(lo, b_lo * HKV), min(hi, b_hi * HKV)):
         b, hk = divmod(u, HKV)
         g.manual_seed(seed + u)
         bl = b - b_lo
         q[bl, :, hk * r:(hk + 1) * r] = torch.randn((N, r, D), generator=g, device=device).to(tdt)
-        kk = torch.randn((N, D), generator=g, device=device)
-        if cfg.get("eps", 0.0) > 0:  # GRN: multiplicity-scaled keys, m in {0..5} (cli.py:296; grn.py:150)
-            m = torch.randint(0, 6, (N, 1), generator=g, device=device).float()
-            kk = kk * m
-        k[bl, :, hk] = kk.to(tdt)
+        k[bl, :, hk] = torch.randn((N, D), generator=g, device=device).to(tdt)
         v[bl, :, hk] = torch.randn((N, D), generator=g, device=device).to(tdt)
-    return q, k, v, b_lo * HKV
+    if m is not None:
+        for bl in range(nb):
+            g.manual_seed(seed + 1_000_003 * (b_lo + bl))
+            m[bl] = torch.randint(0, 6, (N,), generator=g, device=device).float()
+    if m is not None and not cfg.get("fused_mult"):
+        k.copy_((k.float() * m[:, :, None, None]).to(tdt))
+        m = None
+    return q, k, v, m, b_lo * HKV
 
 
 def cpu_reference_sample(cfg, rows: int, seed: int = 7):
@@ -244,7 +276,7 @@ def run_ours(args, cfg):
     B, H, HKV, N, D = cfg["B"], cfg["H"], cfg["HKV"], cfg["N"], cfg["D"]
     n_units = B * HKV
     lo, hi = partition.unit_range(n_units, world, rank)
-    q, k, v, u_off = make_inputs(cfg, lo, hi, dev)
+    q, k, v, mult, u_off = make_inputs(cfg, lo, hi, dev)
     out_dtype = torch.bfloat16 if cfg["dtype"] == "e4m3" else q.dtype
     o = torch.empty(q.shape, dtype=out_dtype, device=dev)
     r = H // HKV
@@ -255,7 +287,7 @@ def run_ours(args, cfg):
 
     def step():
         return partition.fwd_shard(q, k, v, o, lo - u_off, hi - u_off,
-                                   lambda *a, **k2: flashsign.fwd_async(*a, bad_key=bad, **k2), **kw)
+                                   lambda *a, **k2: flashsign.fwd_async(*a, bad_key=bad, **k2), key_scale=mult, **kw)
 
     n_launch_per_step = len(partition.pieces(q.shape[0], HKV, lo - u_off, hi - u_off))
     for _ in range(args.warmup):
@@ -293,23 +325,24 @@ def run_ours(args, cfg):
         kh = k.cpu().pin_memory()
         vh = v.cpu().pin_memory()
         oh = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+        mh = None if mult is None else mult.cpu().pin_memory()
         pipe = HostPipeline(dev)
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         for _ in range(min(args.warmup, 2)):
-            pipe.run(qh, kh, vh, oh, check=False, **kw)
+            pipe.run(qh, kh, vh, oh, check=False, key_scale=mh, **kw)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            pipe.run(qh, kh, vh, oh, check=False, **kw)  # run() synchronises: output is on the host
+            pipe.run(qh, kh, vh, oh, check=False, key_scale=mh, **kw)  # run() synchronises: output on the host
         dt = (time.perf_counter() - t0) / e2e_steps
         tt = torch.tensor([dt], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
         elsz = q.element_size()
-        h2d = (q.numel() + k.numel() + v.numel()) * elsz
+        h2d = (q.numel() + k.numel() + v.numel()) * elsz + (0 if mh is None else mh.numel() * 4)
         d2h = o.numel() * o.element_size()
         if world > 1:
             vals = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
@@ -324,6 +357,9 @@ def run_ours(args, cfg):
         fp8 = cfg["dtype"] == "e4m3"
         peak = peaks.get("fp8_tflops") if fp8 else peaks["bf16_tflops"]
         peak_note = "MEASURED_PEAKS.json bf16_tflops (burst)"
+        if fp8 and peak is None:
+            peak = measure_fp8_peak(dev)
+            peak_src, peak_note = "measured", "this run: cuBLASLt torch._scaled_mm e4m3 8192^3, best of 10 (burst)"
         if fp8 and peak is None:
             peak = 2.0 * peaks["bf16_tflops"]
             peak_note = "2 x MEASURED_PEAKS.json bf16_tflops (FP8 dense = 2x BF16; no measured FP8 peak)"
@@ -383,10 +419,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--context", action="store_true", help="also time torch-eager spherical and SDPA")
+    ap.add_argument("--fused-mult", action="store_true", help="c5: fuse the key multiplicities into the kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.fused_mult:
+        if not cfg.get("mult"):
+            ap.error("--fused-mult applies to the GRN configuration (c5) only")
+        cfg["fused_mult"] = True
+        cfg["desc"] += ", fused in-kernel (key_scale)"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

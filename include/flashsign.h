@@ -20,9 +20,11 @@
  *                      (attention.py:86-97, 169-171).
  *   fs_last_error   <- the exception message text.
  *
- * Math (normalizers.py:94-100, SPHERICAL; eps = denom_epsilon, normalizers.py:69):
- *     s_ij = scale * q_descale * k_descale * (q_i . k_j)
- *     O_i  = v_descale * sum_j s_ij v_j / sqrt(sum_j s_ij^2 + eps)
+ * Math (eps = denom_epsilon, normalizers.py:69; m_j = optional key multiplicity,
+ * attention.py:381-388 / grn.py:150, 1 when key_scale is NULL):
+ *     s_ij = scale * q_descale * k_descale * m_j * (q_i . k_j)
+ *     SPHERICAL (normalizers.py:94-100):  O_i = v_descale * sum_j s_ij v_j / sqrt(sum_j s_ij^2 + eps)
+ *     SIGNED_L1 (normalizers.py:111-117): O_i = v_descale * sum_j s_ij v_j / (sum_j |s_ij| + eps)
  *
  * No torch types cross this boundary: plain device pointers, element strides,
  * sizes and a cudaStream_t.  All calls are asynchronous on `stream`.
@@ -54,6 +56,11 @@ typedef enum {
   FS_F32 = 3 /* output only */
 } fs_dtype;
 
+typedef enum {
+  FS_NORM_SPHERICAL = 0, /* a1(u) = u, a2(u) = u^2, b = sqrt  (normalizers.py:94-100)  */
+  FS_NORM_SIGNED_L1 = 1  /* a1(u) = u, a2(u) = |u|, b = id    (normalizers.py:111-117) */
+} fs_normalizer;
+
 /* Sentinel value of *bad_key when no row was degenerate. */
 #define FS_BAD_NONE 0xFFFFFFFFFFFFFFFFull
 
@@ -73,11 +80,20 @@ typedef struct {
   /* Optional device scalar (may be NULL).  fs_fwd resets it to FS_BAD_NONE on
      `stream`, then the kernel atomically keeps the minimum of
        (linear_row << 32) | float_bits(z),  linear_row = (b*heads_q + h)*seqlen_q + n
-     over rows whose denominator sqrt(z + eps) is 0 or non-finite, i.e. the
+     over rows whose denominator b(z + eps) is 0 or non-finite, i.e. the
      first bad row in the reference's loop order (batch, head, row) and its z
-     = sum_j s_ij^2.  An FP16/FP8 P overflow is reported as z = +inf. */
+     = sum_j a2(s_ij).  An FP16/FP8 P overflow is reported as z = +inf. */
   uint64_t *bad_key;
   int32_t tile_m_hint, tile_n_hint; /* TileConfig (g_y, s_x); advisory only    */
+  int32_t normalizer;               /* fs_normalizer; 0 = SPHERICAL            */
+  int32_t reserved0;                /* must be 0                               */
+  /* Optional per-key multiplicity m (NULL: none): fp32 device array [batch, seqlen_kv],
+     element (b, n) at key_scale[b*key_scale_stride + n], shared by all kv heads -- the
+     reference's apply_multiplicity_array(K, m) (attention.py:381-388) fused into the
+     score.  m must be finite and >= 0 (the caller validates; the reference raises
+     ValueError).  16-byte aligned; key_scale_stride*4 a multiple of 16 when batch > 1. */
+  const float *key_scale;
+  int64_t key_scale_stride;
 } fs_fwd_params;
 
 /* Validate, encode TMA descriptors (cached per call), launch.  Async. */

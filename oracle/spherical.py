@@ -15,6 +15,9 @@ Contract (attention.py:1-11, normalizers.py:94-100):
     s_ij = c * (q_i . k_j)
     O_i  = sum_j s_ij v_j / sqrt(sum_j s_ij^2 + eps)
 
+and the other exp-free triple the kernel compiles, SIGNED_L1 (normalizers.py:111-117):
+O_i = sum_j s_ij v_j / (sum_j |s_ij| + eps).  ``norm="signed_l1"`` selects it.
+
 Parity pinning: ``tests/test_oracle.py`` checks every function here against
 golden vectors produced by running the reference itself
 (``tests/golden/make_golden.py`` -> ``tests/golden/*.npz``), including the
@@ -53,8 +56,12 @@ def _check(q, k, v):
         raise ValueError(f"K and V row counts differ: {k.shape} vs {v.shape}")
 
 
+_A2 = {"spherical": lambda s: s * s, "signed_l1": np.abs}       # normalizers.py:97, 114
+_B = {"spherical": np.sqrt, "signed_l1": lambda z: z}          # normalizers.py:98, 115
+
+
 def naive_spherical(q: np.ndarray, k: np.ndarray, v: np.ndarray,
-                    scale: float = 1.0, eps: float = 0.0) -> np.ndarray:
+                    scale: float = 1.0, eps: float = 0.0, norm: str = "spherical") -> np.ndarray:
     """Materialising oracle, restating ``naive_attention_array`` (attention.py:114-143).
 
     float32 inputs: scores accumulate in float64 and round to float32
@@ -69,8 +76,8 @@ def naive_spherical(q: np.ndarray, k: np.ndarray, v: np.ndarray,
         s = q @ k.T
     if scale != 1.0:
         s = s * np.asarray(scale, dtype=s.dtype)
-    z = (s * s).sum(axis=1)
-    den = np.sqrt(z + eps) if eps else np.sqrt(z)
+    z = _A2[norm](s).sum(axis=1)
+    den = _B[norm](z + eps) if eps else _B[norm](z)
     bad = ~np.isfinite(den) | (den == 0)
     if bad.any():
         row = int(np.argmax(bad))
@@ -89,9 +96,10 @@ def quantize_f16(a: np.ndarray) -> np.ndarray:
 
 def streamed_spherical(q: np.ndarray, k: np.ndarray, v: np.ndarray,
                        scale: float = 1.0, eps: float = 0.0,
-                       g_y: int = 64, s_x: int = 64, f16: bool = False) -> np.ndarray:
+                       g_y: int = 64, s_x: int = 64, f16: bool = False, norm: str = "spherical") -> np.ndarray:
     """The FlashSign tile loop, restating ``streamed_attention_array`` +
-    ``_streamed_tiles`` spherical branch (attention.py:252-279, 146-200).
+    ``_streamed_tiles`` non-safe branch (attention.py:252-279, 146-200) for the
+    exp-free triples (``norm``: spherical | signed_l1).
 
     Query groups of ``g_y`` rows; K/V chunks of ``s_x`` keys; per-row (o, z)
     accumulators in float64 (float32 under f16 emulation, 157-158); scores
@@ -130,10 +138,10 @@ def streamed_spherical(q: np.ndarray, k: np.ndarray, v: np.ndarray,
                 o += st @ v64[c0:c1].astype(np.float32)
             else:
                 o += st.astype(np.float64, copy=False) @ v64[c0:c1]
-            z += (st * st).sum(axis=1, dtype=z.dtype)
+            z += _A2[norm](st).sum(axis=1, dtype=z.dtype)
             if f16:
                 o = quantize_f16(o)
-        den = np.sqrt(z + eps) if eps else np.sqrt(z)
+        den = _B[norm](z + eps) if eps else _B[norm](z)
         bad = ~np.isfinite(den) | (den == 0)
         if bad.any():
             i = int(np.argmax(bad))
@@ -144,7 +152,7 @@ def streamed_spherical(q: np.ndarray, k: np.ndarray, v: np.ndarray,
 
 def multi_head_spherical(q: np.ndarray, k: np.ndarray, v: np.ndarray, h: int, h_kv: int,
                          scale: float = 1.0, eps: float = 0.0, path: str = "streamed",
-                         g_y: int = 64, s_x: int = 64, f16: bool = False) -> np.ndarray:
+                         g_y: int = 64, s_x: int = 64, f16: bool = False, norm: str = "spherical") -> np.ndarray:
     """GQA over ``[n, heads, d]``, restating ``multi_head_attention_array``
     (attention.py:318-361): query head i reads kv head (i*h_kv)//h (352), heads
     run serially (351) so the first degenerate head in loop order raises."""
@@ -155,9 +163,9 @@ def multi_head_spherical(q: np.ndarray, k: np.ndarray, v: np.ndarray, h: int, h_
         kv = (i * h_kv) // h
         try:
             if path == "streamed":
-                out[:, i, :] = streamed_spherical(q[:, i], k[:, kv], v[:, kv], scale, eps, g_y, s_x, f16)
+                out[:, i, :] = streamed_spherical(q[:, i], k[:, kv], v[:, kv], scale, eps, g_y, s_x, f16, norm)
             else:
-                out[:, i, :] = naive_spherical(q[:, i], k[:, kv], v[:, kv], scale, eps)
+                out[:, i, :] = naive_spherical(q[:, i], k[:, kv], v[:, kv], scale, eps, norm)
         except OracleDegenerate as e:
             e.head = i
             raise
@@ -193,15 +201,44 @@ def gram_spherical(q: np.ndarray, k: np.ndarray, v: np.ndarray,
 
 
 def gram_batched(q: np.ndarray, k: np.ndarray, v: np.ndarray,
-                 scale: float = 1.0, eps: float = 0.0) -> np.ndarray:
-    """``gram_spherical`` over BSHD ``[B, N, H, d]`` with GQA (h -> h*H_kv//H)."""
+                 scale: float = 1.0, eps: float = 0.0, m: np.ndarray | None = None) -> np.ndarray:
+    """``gram_spherical`` over BSHD ``[B, N, H, d]`` with GQA (h -> h*H_kv//H).
+    ``m`` [B, Nkv]: key multiplicities, K' = m K (attention.py:381-388) in float64."""
     b_, n_q, h_, d = q.shape
     h_kv = k.shape[2]
     out = np.empty(q.shape, dtype=np.float64)
     for b in range(b_):
         for h in range(h_):
             kv = (h * h_kv) // h_
-            out[b, :, h] = gram_spherical(q[b, :, h], k[b, :, kv], v[b, :, kv], scale, eps)
+            kb = np.asarray(k[b, :, kv], dtype=np.float64)
+            if m is not None:
+                kb = kb * np.asarray(m[b], dtype=np.float64)[:, None]
+            out[b, :, h] = gram_spherical(q[b, :, h], kb, v[b, :, kv], scale, eps)
+    return out
+
+
+def exact_batched(q: np.ndarray, k: np.ndarray, v: np.ndarray, scale: float = 1.0, eps: float = 0.0,
+                  norm: str = "spherical", m: np.ndarray | None = None) -> np.ndarray:
+    """float64 oracle over BSHD with GQA for either exp-free triple: the Gram form for
+    spherical, the materialised scores (attention.py:114-143 in float64) for signed_l1.
+    Degenerate rows come back as NaN."""
+    if norm == "spherical":
+        return gram_batched(q, k, v, scale, eps, m)
+    b_, n_q, h_, d = q.shape
+    h_kv = k.shape[2]
+    out = np.empty(q.shape, dtype=np.float64)
+    for b in range(b_):
+        for h in range(h_):
+            kv = (h * h_kv) // h_
+            kb = np.asarray(k[b, :, kv], dtype=np.float64)
+            if m is not None:
+                kb = kb * np.asarray(m[b], dtype=np.float64)[:, None]
+            s = scale * (np.asarray(q[b, :, h], dtype=np.float64) @ kb.T)
+            den = _A2[norm](s).sum(axis=1) + eps
+            with np.errstate(divide="ignore", invalid="ignore"):
+                o = (s @ np.asarray(v[b, :, kv], dtype=np.float64)) / den[:, None]
+            o[den == 0] = np.nan
+            out[b, :, h] = o
     return out
 
 

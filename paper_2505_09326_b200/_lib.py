@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libflashsign.so")
 
 FS_OK, FS_ERR_SHAPE, FS_ERR_CONFIG, FS_ERR_DTYPE, FS_ERR_UNSUPPORTED, FS_ERR_CUDA = range(6)
 FS_F16, FS_BF16, FS_E4M3, FS_F32 = range(4)
+FS_NORM_SPHERICAL, FS_NORM_SIGNED_L1 = range(2)
 FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
 
 # every symbol include/flashsign.h declares
@@ -51,6 +52,10 @@ class FsFwdParams(ctypes.Structure):
         ("bad_key", ctypes.c_void_p),
         ("tile_m_hint", ctypes.c_int32),
         ("tile_n_hint", ctypes.c_int32),
+        ("normalizer", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
+        ("key_scale", ctypes.c_void_p),
+        ("key_scale_stride", ctypes.c_int64),
     ]
 
 

@@ -47,7 +47,8 @@ __all__ = [
     "ConfigError", "TileConfig", "AttentionConfig", "ScoreBufferMeter", "default_score_scale",
     "naive_attention_array", "streamed_attention_array", "naive_generalized_attention",
     "streamed_attention", "multi_head_attention_array", "multi_head_attention",
-    "apply_multiplicity_array", "apply_multiplicity", "set_compute_dtype", "get_compute_dtype",
+    "apply_multiplicity_array", "apply_multiplicity", "multiplicity_attention_array",
+    "set_compute_dtype", "get_compute_dtype",
 ]
 
 _COMPUTE_DTYPES = {"fp16": torch.float16, "bf16": torch.bfloat16}
@@ -143,10 +144,13 @@ def _device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _require_spherical(spec) -> None:
-    if getattr(spec, "name", None) != "spherical":
-        raise ConfigError(f"flashsign: only the spherical normaliser runs on the GPU streamed path, "
-                          f"got {getattr(spec, 'name', spec)!r}")
+def _gpu_normalizer(spec) -> str:
+    """The exp-free triples run on the kernel (spherical, signed_l1); softmax is not FlashSign."""
+    name = getattr(spec, "name", None)
+    if name not in flashsign.NORMALIZERS:
+        raise ConfigError(f"flashsign: the GPU streamed path runs the exp-free normalisers "
+                          f"{sorted(flashsign.NORMALIZERS)}, got {getattr(spec, 'name', spec)!r}")
+    return name
 
 
 def _out_dtype(a: np.ndarray):
@@ -154,7 +158,8 @@ def _out_dtype(a: np.ndarray):
 
 
 def _to_device(a: np.ndarray, dev, dtype: torch.dtype, d_pad: int) -> torch.Tensor:
-    t = torch.from_numpy(np.ascontiguousarray(a))
+    a = np.ascontiguousarray(a)
+    t = torch.from_numpy(a if a.flags.writeable else a.copy())
     if t.dtype not in (torch.float16, torch.float32, torch.float64):
         t = t.to(torch.float64)
     t = t.to(dev, non_blocking=False)
@@ -166,7 +171,7 @@ def _to_device(a: np.ndarray, dev, dtype: torch.dtype, d_pad: int) -> torch.Tens
 
 
 def _gpu_streamed(q3: np.ndarray, k3: np.ndarray, v3: np.ndarray, scale: float, eps: float,
-                  compute: str, meter) -> np.ndarray:
+                  compute: str, meter, normalizer: str = "spherical", m: np.ndarray | None = None) -> np.ndarray:
     """FlashSign on [n, h, d] / [x, h_kv, d] arrays in one launch; raises the
     reference's DegenerateDenominatorError for the first bad (head, row)."""
     n, h, d = q3.shape
@@ -191,7 +196,11 @@ def _gpu_streamed(q3: np.ndarray, k3: np.ndarray, v3: np.ndarray, scale: float, 
     if x == 0:  # keep TMA descriptors valid for an empty K/V stream
         kt = torch.zeros((1, 1, h_kv, d_pad), dtype=tdt, device=dev)[:, :0]
         vt = kt
-    o, bad = flashsign.fwd_async(qt, kt, vt, scale=float(scale), eps=float(eps), out_dtype=torch.float32)
+    ks = None
+    if m is not None and x > 0:
+        ks = torch.from_numpy(np.ascontiguousarray(m, dtype=np.float32)).to(dev)[None]
+    o, bad = flashsign.fwd_async(qt, kt, vt, scale=float(scale), eps=float(eps), out_dtype=torch.float32,
+                                 normalizer=normalizer, key_scale=ks)
     info = flashsign.decode_bad_key(int(bad.item()), h, n)
     if info is not None:
         _, _, row, z = info
@@ -203,7 +212,7 @@ def streamed_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: 
                              tile: TileConfig, f16: bool = False, meter: ScoreBufferMeter | None = None) -> np.ndarray:
     """Streamed path on plain arrays (attention.py:252-279), on the FlashSign kernel."""
     _check_qkv(q, k, v)
-    _require_spherical(spec)
+    norm = _gpu_normalizer(spec)
     if tile.g_y < 1 or tile.s_x < 1:
         raise ConfigError(f"tile sizes must be >= 1, got g_y={tile.g_y}, s_x={tile.s_x}")
     compute = _compute
@@ -211,7 +220,8 @@ def streamed_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: 
         if q.dtype != np.float32:
             raise ConfigError("f16 emulation requires float32 inputs")
         compute = "fp16"
-    out = _gpu_streamed(q[:, None, :], k[:, None, :], v[:, None, :], scale, spec.denom_epsilon, compute, meter)
+    out = _gpu_streamed(q[:, None, :], k[:, None, :], v[:, None, :], scale, spec.denom_epsilon, compute, meter,
+                        norm)
     return out[:, 0, :]
 
 
@@ -245,7 +255,7 @@ def multi_head_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec
         raise ShapeMismatchError(f"Q and K feature dims differ: {q.shape} vs {k.shape}")
     if k.shape[0] != v.shape[0]:
         raise ShapeMismatchError(f"K and V row counts differ: {k.shape} vs {v.shape}")
-    _require_spherical(spec)
+    norm = _gpu_normalizer(spec)
     if eff_tile.g_y < 1 or eff_tile.s_x < 1:
         raise ConfigError("tile sizes must be >= 1")
     compute = _compute
@@ -253,7 +263,47 @@ def multi_head_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec
         if q.dtype != np.float32:
             raise ConfigError("f16 emulation requires float32 inputs")
         compute = "fp16"
-    return _gpu_streamed(q, k, v, eff_scale, spec.denom_epsilon, compute, meter)
+    return _gpu_streamed(q, k, v, eff_scale, spec.denom_epsilon, compute, meter, norm)
+
+
+def multiplicity_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, m, spec: NormalizerSpec, h: int,
+                                 h_kv: int, scale: float | None = None, tile: TileConfig | None = None,
+                                 f16: bool = False, meter: ScoreBufferMeter | None = None) -> np.ndarray:
+    """The GRN layer's attention call with the key multiplicities fused into the kernel:
+
+        multi_head_attention_array(q, apply_multiplicity_array(k, m), v, spec, h, h_kv, ...)
+
+    (grn.py:150 + 171-173; attention.py:381-388, 318-361) without materialising K' = m K:
+    the kernel scales each score, s_ij -> m_j s_ij, in fp32.  Same validation and errors
+    as the two reference calls (ShapeMismatchError for a length mismatch, ValueError for
+    negative or non-finite m).
+    """
+    mv = np.asarray(m, dtype=np.float64)
+    if mv.ndim != 1 or k.ndim < 1 or mv.shape[0] != k.shape[0]:
+        raise ShapeMismatchError(f"multiplicity length {mv.shape} does not match {k.shape[0]} rows")
+    if not np.isfinite(mv).all() or (mv < 0).any():
+        raise ValueError("multiplicities must be finite and nonnegative")
+    if h < 1 or h_kv < 1 or h % h_kv != 0:
+        raise ConfigError(f"query heads must be a multiple of kv heads, got h={h}, h_kv={h_kv}")
+    if q.ndim != 3 or k.ndim != 3 or v.ndim != 3:
+        raise ShapeMismatchError(f"expected rank-3 inputs, got {q.shape}, {k.shape}, {v.shape}")
+    if q.shape[1] != h or k.shape[1] != h_kv or v.shape[1] != h_kv:
+        raise ShapeMismatchError(f"head axes do not match h={h}, h_kv={h_kv}: {q.shape}, {k.shape}, {v.shape}")
+    if q.shape[2] != k.shape[2]:
+        raise ShapeMismatchError(f"Q and K feature dims differ: {q.shape} vs {k.shape}")
+    if k.shape[0] != v.shape[0]:
+        raise ShapeMismatchError(f"K and V row counts differ: {k.shape} vs {v.shape}")
+    norm = _gpu_normalizer(spec)
+    eff_scale = scale if scale is not None else default_score_scale(spec, q.shape[2])
+    eff_tile = tile if tile is not None else TileConfig()
+    if eff_tile.g_y < 1 or eff_tile.s_x < 1:
+        raise ConfigError("tile sizes must be >= 1")
+    compute = _compute
+    if f16:
+        if q.dtype != np.float32:
+            raise ConfigError("f16 emulation requires float32 inputs")
+        compute = "fp16"
+    return _gpu_streamed(q, k, v, eff_scale, spec.denom_epsilon, compute, meter, norm, mv)
 
 
 def naive_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: NormalizerSpec, scale: float,

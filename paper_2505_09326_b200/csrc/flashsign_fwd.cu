@@ -97,11 +97,11 @@ struct KParams {
   int32_t heads_q, heads_kv, seqlen_q, seqlen_kv, head_dim;
   int32_t n_qblk;   // work tiles per (batch, head) = ceil(seqlen_q / (NQT*BM))
   int32_t n_tiles;  // n_qblk * heads_q * batch
-  float g2;         // (scale * q_descale * k_descale)^2
+  float zmul;       // spherical: (scale*q_descale*k_descale)^2; signed L1: |scale*q_descale*k_descale|
   float out_mul;    // scale * q_descale * k_descale * v_descale / p_scale
   float eps;
   float p_scale;
-  float ovf_z;      // (PMAX / |p_scale|)^2: a P-tile half whose sum of s^2 stays below cannot overflow
+  float ovf_z;      // a P chunk whose sum of a2(s) stays below this cannot overflow (PMAX/|p_scale|)^{2|1}
   uint64_t* bad_key;
 };
 
@@ -151,7 +151,10 @@ struct Cfg {
   static constexpr int NSB = (FS_NSB3 && 3 * BN + NQT * D <= TMEM_COLS) ? 3 : 2;
   // O accumulators double-buffered in TMEM when they still fit: the epilogue never gates the MMAs.
   static constexpr int NOB = (FS_NOB2 && NSB * BN + 2 * NQT * D <= TMEM_COLS) ? 2 : 1;
-  static constexpr int SMEM_BYTES = ZBUF_OFF + NQT * NOB * 2 * BM * 4 + 1024;  // + alignment slack
+  // per-key multiplicities m_j of each V slot's keys (fused K' = m K, grn.py:150)
+  static constexpr int MS_OFF = ZBUF_OFF + NQT * NOB * 2 * BM * 4;
+  static constexpr int MS_SLOT_BYTES = BN * 4;
+  static constexpr int SMEM_BYTES = MS_OFF + STAGES * MS_SLOT_BYTES + 1024;  // + alignment slack
   static constexpr int QK_STEPS = ROW_BYTES / 32;                          // 32 B of K-dim per MMA
   static constexpr int PV_STEPS = BN / TR::KSTEP;
   static constexpr uint32_t COL_S0 = 0;
@@ -244,10 +247,13 @@ __device__ __forceinline__ TileCoord decode_tile(int tile, const KParams& p) {
   return c;
 }
 
-template <int IN, int D, int OUT>
+// NORM: FS_NORM_SPHERICAL (a2 = s^2, b = sqrt) | FS_NORM_SIGNED_L1 (a2 = |s|, b = id), normalizers.py:94-117.
+// KS: per-key multiplicity scale m_j fused into the score (s_ij -> m_j s_ij), attention.py:381-388.
+template <int IN, int D, int OUT, int NORM, bool KS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     flashsign_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                         const __grid_constant__ CUtensorMap tm_v, const KParams p) {
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_m,
+                         const KParams p) {
   using C = Cfg<IN, D>;
   using TR = InTraits<IN>;
   extern __shared__ uint8_t smem_raw[];
@@ -291,6 +297,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
+    if (KS) ptx::tma_prefetch_desc(&tm_m);
   }
   if (warp == 2) ptx::tmem_alloc(&bars->tmem_base, TMEM_COLS);
   ptx::tc_fence_before();
@@ -333,9 +340,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t slot = kv_i % C::STAGES;
           const uint32_t round = kv_i / C::STAGES;
           ptx::mbar_wait(&bars->kv_empty[slot], (round & 1u) ^ 1u);
-          ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::SLOT_BYTES);
+          const bool with_m = KS && (i & 1);  // V slots also carry the tile's key multiplicities
+          ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::SLOT_BYTES + (with_m ? C::MS_SLOT_BYTES : 0));
           const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
           const int key0 = (i >> 1) * BN;
+          if (with_m)
+            ptx::tma_load_2d(smem + C::MS_OFF + slot * C::MS_SLOT_BYTES, &tm_m, &bars->kv_full[slot], key0,
+                             tc.batch, pol_kv);
 #pragma unroll
           for (int db = 0; db < C::NDB; ++db)
             ptx::tma_load_4d(smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128), tm, &bars->kv_full[slot],
@@ -624,8 +635,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // S allocation u = 2*jg + t lives in buffer u % NSB (see the MMA issuer)
         const uint32_t u = 2u * s_use + t, sb = u % C::NSB;
         ptx::mbar_wait(&bars->s_full[sb], (u / C::NSB) & 1u);
-        ++s_use;
         const uint32_t s_base = s_lane + sb * BN;
+        // key multiplicities of this K/V tile ride in V_j's ring slot; that slot is released only
+        // after PV_1(j), which needs this warp's P, so they stay valid while they are read here
+        const uint32_t v_idx = 2u * s_use + 1u, v_slot = v_idx % C::STAGES;
+        if constexpr (KS) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
+        ++s_use;
 #if FS_PROF
         const long long tn1 = clock64();
         pr_sw += tn1 - tn0;
@@ -642,19 +657,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
-          // sum of squares: packed FP32 FMAs, two independent chains
+          // sum of a2(s): packed FP32 FMAs / adds, two independent chains.  With KS the scores are
+          // first scaled by the key multiplicities, s_ij <- m_j s_ij (fp32; exact for integer m).
+          const float4* mp = reinterpret_cast<const float4*>(smem + C::MS_OFF + v_slot * C::MS_SLOT_BYTES) +
+                             (hh * (BN / 2) + ch * 32) / 4;
           float2 h0 = make_float2(0.f, 0.f), h1 = h0;
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float2 a = make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1]));
-            const float2 b = make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
-            h0 = __ffma2_rn(a, a, h0);
-            h1 = __ffma2_rn(b, b, h1);
+            float2 a = make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1]));
+            float2 b = make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+            if constexpr (KS) {
+              const float4 m4 = mp[i / 4];
+              a = __fmul2_rn(a, make_float2(m4.x, m4.y));
+              b = __fmul2_rn(b, make_float2(m4.z, m4.w));
+              s[i + 0] = __float_as_uint(a.x);
+              s[i + 1] = __float_as_uint(a.y);
+              s[i + 2] = __float_as_uint(b.x);
+              s[i + 3] = __float_as_uint(b.y);
+            }
+            if constexpr (NORM == FS_NORM_SIGNED_L1) {
+              h0 = __fadd2_rn(h0, make_float2(fabsf(a.x), fabsf(a.y)));
+              h1 = __fadd2_rn(h1, make_float2(fabsf(b.x), fabsf(b.y)));
+            } else {
+              h0 = __ffma2_rn(a, a, h0);
+              h1 = __ffma2_rn(b, b, h1);
+            }
           }
           za = __fadd2_rn(za, h0);
           zb = __fadd2_rn(zb, h1);
           if constexpr (TR::CHECK_OVF) {
-            // max|s| <= sqrt(sum s^2): only a chunk whose sum reaches (PMAX/|ps|)^2 can overflow P
+            // max|s| <= sqrt(sum s^2) (<= sum |s|): only a chunk whose sum reaches ovf_z can overflow P
             const float zh = (h0.x + h0.y) + (h1.x + h1.y);
             if (zh >= p.ovf_z) {
               float amax = 0.f;
@@ -726,16 +758,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
 #pragma unroll 1
       for (int t = 0; t < NQT; ++t) {
-        // zr = sum_j (c s_ij)^2 (what the reference calls z), or +inf for a P overflow
+        // zr = sum_j a2(c s_ij) (what the reference calls z), or +inf for a P overflow
         float zr = 0.f;
         if (n_kv_tiles > 0) {
           ptx::mbar_wait(&bars->z_full[t][ob], o_use & 1u);
           const float* zt = zbuf + (t * C::NOB + ob) * 2 * BM + r;
-          zr = p.g2 * (zt[0] + zt[BM]);  // the two column halves of the row
+          zr = p.zmul * (zt[0] + zt[BM]);  // the two column halves of the row
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&bars->z_empty[t][ob]);
         }
-        const float den = sqrtf(zr + p.eps);
+        const float den = NORM == FS_NORM_SIGNED_L1 ? zr + p.eps : sqrtf(zr + p.eps);
         const bool bad = !(den > 0.f) || isinf(den);
         const float mul = __fdiv_rn(p.out_mul, den);
         const int row = tc.qblk * (NQT * BM) + t * BM + r;
@@ -828,6 +860,29 @@ static bool encode_bshd(CUtensorMap* map, CUtensorMapDataType dt, int eb, const 
   return true;
 }
 
+// Key multiplicities m [batch, seqlen_kv] fp32 (token stride 1): 128-key boxes, zero-filled past
+// seqlen_kv so padded keys stay exactly zero.
+static bool encode_key_scale(CUtensorMap* map, const fs_fwd_params* p, std::string* err) {
+  auto enc = get_encode_fn();
+  if (!enc) {
+    *err = "cuTensorMapEncodeTiled unavailable (driver too old?)";
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)(p->seqlen_kv > 0 ? p->seqlen_kv : 1), (cuuint64_t)p->batch};
+  const int64_t sb = p->batch > 1 ? p->key_scale_stride : ((p->seqlen_kv + 3) / 4) * 4;
+  cuuint64_t strides[1] = {(cuuint64_t)(sb * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)BN, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p->key_scale), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled (key_scale) failed with CUresult " + std::to_string((int)r);
+    return false;
+  }
+  return true;
+}
+
 // SM count of the current device (persistent grid size), cached per device.
 static int num_sms() {
   static int cache[64] = {0};
@@ -845,10 +900,10 @@ static int num_sms() {
   return cache[dev];
 }
 
-template <int IN, int D, int OUT>
+template <int IN, int D, int OUT, int NORM, bool KS>
 static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   using C = Cfg<IN, D>;
-  auto kern = flashsign_fwd_kernel<IN, D, OUT>;
+  auto kern = flashsign_fwd_kernel<IN, D, OUT, NORM, KS>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -868,6 +923,8 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
       !encode_bshd(&tv, dt, C::EB, p->v, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->v_stride, C::BOXW,
                    &err))
     return fail(FS_ERR_UNSUPPORTED, err);
+  CUtensorMap tm = tq;  // unused unless KS
+  if (KS && !encode_key_scale(&tm, p, &err)) return fail(FS_ERR_UNSUPPORTED, err);
 
   KParams kp;
   kp.o = p->o;
@@ -880,13 +937,13 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   kp.seqlen_kv = p->seqlen_kv;
   kp.head_dim = p->head_dim;
   const double g = (double)p->scale * p->q_descale * p->k_descale;
-  kp.g2 = (float)(g * g);
+  kp.zmul = (float)(NORM == FS_NORM_SIGNED_L1 ? std::fabs(g) : g * g);
   kp.out_mul = (float)(g * p->v_descale / p->p_scale);
   kp.eps = p->eps;
   kp.p_scale = p->p_scale;
   kp.bad_key = p->bad_key;
   const double pmax = InTraits<IN>::PMAX / std::fabs((double)p->p_scale);
-  kp.ovf_z = (float)std::fmin(pmax * pmax, 3.0e38);
+  kp.ovf_z = (float)std::fmin(NORM == FS_NORM_SIGNED_L1 ? pmax : pmax * pmax, 3.0e38);
   const int64_t n_qblk = (p->seqlen_q + NQT * BM - 1) / (NQT * BM);
   const int64_t n_tiles = n_qblk * p->heads_q * p->batch;
   if (n_tiles > INT32_MAX) return fail(FS_ERR_UNSUPPORTED, "too many work tiles for one launch");
@@ -894,24 +951,32 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   kp.n_tiles = (int32_t)n_tiles;
   const int grid = (int)std::min<int64_t>(n_tiles, num_sms());
   if (grid <= 0) return fail(FS_ERR_CUDA, "no SMs reported for the current device");
-  kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, kp);
+  kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, tm, kp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   return FS_OK;
 }
 
-template <int IN, int D>
+template <int IN, int D, int NORM, bool KS>
 static fs_status dispatch_out(const fs_fwd_params* p, cudaStream_t s) {
   switch (p->out_dtype) {
     case FS_F32:
-      return launch<IN, D, FS_F32>(p, s);
+      return launch<IN, D, FS_F32, NORM, KS>(p, s);
     case FS_BF16:
-      return launch<IN, D, FS_BF16>(p, s);
+      return launch<IN, D, FS_BF16, NORM, KS>(p, s);
     case FS_F16:
-      return launch<IN, D, FS_F16>(p, s);
+      return launch<IN, D, FS_F16, NORM, KS>(p, s);
     default:
       return fail(FS_ERR_DTYPE, "out_dtype must be FS_F32, FS_BF16 or FS_F16");
   }
+}
+
+template <int IN, int D>
+static fs_status dispatch_norm(const fs_fwd_params* p, cudaStream_t s) {
+  const bool ks = p->key_scale != nullptr;
+  if (p->normalizer == FS_NORM_SIGNED_L1)
+    return ks ? dispatch_out<IN, D, FS_NORM_SIGNED_L1, true>(p, s) : dispatch_out<IN, D, FS_NORM_SIGNED_L1, false>(p, s);
+  return ks ? dispatch_out<IN, D, FS_NORM_SPHERICAL, true>(p, s) : dispatch_out<IN, D, FS_NORM_SPHERICAL, false>(p, s);
 }
 
 }  // namespace fs
@@ -921,11 +986,11 @@ static fs_status fs_fwd_dispatch(const fs_fwd_params* p, cudaStream_t stream) {
 
   if (p->in_dtype == FS_E4M3) {
     // 1-byte rows: the SW128 layout needs 128-byte rows -> D = 128 (TMA zero-fills d >= head_dim).
-    return dispatch_out<FS_E4M3, 128>(p, stream);
+    return dispatch_norm<FS_E4M3, 128>(p, stream);
   }
   const bool d64 = p->head_dim <= 64;
-  if (p->in_dtype == FS_BF16) return d64 ? dispatch_out<FS_BF16, 64>(p, stream) : dispatch_out<FS_BF16, 128>(p, stream);
-  return d64 ? dispatch_out<FS_F16, 64>(p, stream) : dispatch_out<FS_F16, 128>(p, stream);
+  if (p->in_dtype == FS_BF16) return d64 ? dispatch_norm<FS_BF16, 64>(p, stream) : dispatch_norm<FS_BF16, 128>(p, stream);
+  return d64 ? dispatch_norm<FS_F16, 64>(p, stream) : dispatch_norm<FS_F16, 128>(p, stream);
 }
 
 
@@ -942,7 +1007,7 @@ int fs_prof_read(unsigned long long* out8) {
 
 const char* fs_last_error(void) { return fs::g_last_error.c_str(); }
 
-int fs_version(void) { return 100; }
+int fs_version(void) { return 200; }
 
 int fs_query_tile(int head_dim, fs_dtype dt, int* bm, int* bn) {
   if (!bm || !bn || head_dim < 1 || head_dim > 128) return 1;
@@ -984,6 +1049,13 @@ fs_status fs_fwd(const fs_fwd_params* p, fs_stream_t stream_) {
         (p->o_stride[i] * ob) % 16)
       return fail(FS_ERR_UNSUPPORTED, "batch/token/head strides must be multiples of 16 bytes");
   }
+  if (p->normalizer != FS_NORM_SPHERICAL && p->normalizer != FS_NORM_SIGNED_L1)
+    return fail(FS_ERR_CONFIG, "normalizer must be FS_NORM_SPHERICAL or FS_NORM_SIGNED_L1");
+  if (p->key_scale) {
+    if (!aligned16(p->key_scale)) return fail(FS_ERR_UNSUPPORTED, "key_scale must be 16-byte aligned");
+    if (p->batch > 1 && (p->key_scale_stride < p->seqlen_kv || (p->key_scale_stride * 4) % 16 != 0))
+      return fail(FS_ERR_UNSUPPORTED, "key_scale_stride must be >= seqlen_kv and a multiple of 4 elements");
+  }
   if (p->bad_key) {
     cudaError_t e = cudaMemsetAsync(p->bad_key, 0xFF, sizeof(uint64_t), stream);
     if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
@@ -994,6 +1066,7 @@ fs_status fs_fwd(const fs_fwd_params* p, fs_stream_t stream_) {
     // Empty K/V stream: nothing is loaded, every row has z = 0.  The TMA maps still need a
     // valid global address, so describe K/V over q's storage (never dereferenced).
     fs_fwd_params p2 = *p;
+    p2.key_scale = nullptr;  // nothing is streamed: multiplicities are irrelevant
     p2.k = p2.v = p->q;
     for (int i = 0; i < 3; ++i) p2.k_stride[i] = p2.v_stride[i] = p->q_stride[i];
     p2.heads_kv = p->heads_q;

@@ -1,5 +1,11 @@
 """Torch-native FlashSign forward: CUDA tensors in, CUDA tensor out, one launch.
 
+Normalisers (``normalizer=``): ``"spherical"`` (the FlashSign contract,
+normalizers.py:94-100) and ``"signed_l1"`` (normalizers.py:111-117, a2 = |u|,
+b = identity) -- both exp-free, compiled into the same kernel.  ``key_scale``
+fuses the GRN caller's ``apply_multiplicity_array(K, m)`` (attention.py:381-388,
+grn.py:150) into the score: s_ij -> m_j s_ij.
+
 ``fwd(q, k, v)`` takes BSHD tensors ``q [B, Nq, H, d]``, ``k, v [B, Nkv, H_kv, d]``
 (d contiguous, ``H % H_kv == 0``) in bf16 / fp16 / float8_e4m3fn and calls the
 C-ABI ``fs_fwd`` (include/flashsign.h) on the caller's current CUDA stream.
@@ -31,6 +37,7 @@ _IN_CODES = {torch.bfloat16: _lib.FS_BF16, torch.float16: _lib.FS_F16}
 if hasattr(torch, "float8_e4m3fn"):
     _IN_CODES[torch.float8_e4m3fn] = _lib.FS_E4M3
 _OUT_CODES = {torch.float32: _lib.FS_F32, torch.bfloat16: _lib.FS_BF16, torch.float16: _lib.FS_F16}
+NORMALIZERS = {"spherical": _lib.FS_NORM_SPHERICAL, "signed_l1": _lib.FS_NORM_SIGNED_L1}
 
 _STATUS_EXC = {
     _lib.FS_ERR_SHAPE: ShapeMismatchError,
@@ -72,13 +79,19 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
               out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None, p_scale: float = 1.0,
               q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0,
               bad_key: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
-              tile_hint: tuple[int, int] = (0, 0)):
+              tile_hint: tuple[int, int] = (0, 0), normalizer: str = "spherical",
+              key_scale: torch.Tensor | None = None):
     """Launch FlashSign and return ``(o, bad_key)`` without synchronising.
 
     ``bad_key`` is a 1-element int64 CUDA tensor holding the packed first bad
     row (see ``decode_bad_key``); it may be passed in to avoid an allocation.
+    ``key_scale`` (optional): float32 CUDA tensor ``[B, Nkv]`` (or ``[Nkv]`` when
+    B == 1) of per-key multiplicities, finite and >= 0 -- not validated here
+    (``fwd(check=True)`` does, like attention.py:386-387).
     """
     _check_inputs(q, k, v)
+    if normalizer not in NORMALIZERS:
+        raise ConfigError(f"flashsign: normalizer must be one of {sorted(NORMALIZERS)} (exp-free), got {normalizer!r}")
     if not math.isfinite(scale):
         raise ConfigError(f"score_scale must be finite, got {scale}")
     b, nq, h, d = q.shape
@@ -108,6 +121,17 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
     prm.q_descale, prm.k_descale, prm.v_descale = float(q_descale), float(k_descale), float(v_descale)
     prm.bad_key = bad_key.data_ptr()
     prm.tile_m_hint, prm.tile_n_hint = int(tile_hint[0]), int(tile_hint[1])
+    prm.normalizer = NORMALIZERS[normalizer]
+    if key_scale is not None:
+        ks = key_scale if key_scale.dim() == 2 else key_scale.reshape(1, -1)
+        if (not ks.is_cuda or ks.dtype != torch.float32 or ks.device != q.device
+                or tuple(ks.shape) != (b, nkv) or (nkv > 0 and ks.stride(1) != 1)):
+            raise ShapeMismatchError(f"flashsign: key_scale must be float32 [{b}, {nkv}] on {q.device} with unit "
+                                     f"key stride, got {tuple(key_scale.shape)} {key_scale.dtype}")
+        if (b > 1 and (ks.stride(0) * 4) % 16 != 0) or ks.data_ptr() % 16 != 0:
+            ks = _padded_rows(ks)
+        prm.key_scale, prm.key_scale_stride = ks.data_ptr(), ks.stride(0)
+        key_scale = ks  # keep alive until the launch is enqueued
 
     if stream is None:
         with torch.cuda.device(q.device):
@@ -117,6 +141,20 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
     if st != _lib.FS_OK:
         raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
     return out, bad_key
+
+
+def _padded_rows(ks: torch.Tensor) -> torch.Tensor:
+    """Copy ``ks`` into 16-byte-aligned rows (TMA needs 16-byte row strides)."""
+    b, n = ks.shape
+    buf = torch.zeros((b, max(4, -(-n // 4) * 4)), dtype=torch.float32, device=ks.device)
+    buf[:, :n] = ks
+    return buf[:, :n]
+
+
+def check_key_scale(key_scale: torch.Tensor) -> None:
+    """attention.py:386-387: multiplicities must be finite and nonnegative (synchronises)."""
+    if key_scale.numel() and bool((~torch.isfinite(key_scale) | (key_scale < 0)).any()):
+        raise ValueError("multiplicities must be finite and nonnegative")
 
 
 def decode_bad_key(key: int, heads_q: int, seqlen_q: int):
@@ -141,10 +179,15 @@ def raise_if_bad(bad_key: torch.Tensor, heads_q: int, seqlen_q: int):
 
 def fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float = 1.0, eps: float = 0.0,
         out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None, p_scale: float = 1.0,
-        q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0, check: bool = True) -> torch.Tensor:
-    """FlashSign forward ``O = c*sum_j s_ij v_j / sqrt(c^2 sum_j s_ij^2 + eps)`` on BSHD CUDA tensors."""
+        q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0, check: bool = True,
+        normalizer: str = "spherical", key_scale: torch.Tensor | None = None) -> torch.Tensor:
+    """FlashSign forward ``O = c*sum_j s_ij v_j / sqrt(c^2 sum_j s_ij^2 + eps)`` on BSHD CUDA tensors
+    (``normalizer="signed_l1"``: ``/ (|c| sum_j |s_ij| + eps)``)."""
+    if check and key_scale is not None:
+        check_key_scale(key_scale)
     o, bad = fwd_async(q, k, v, scale=scale, eps=eps, out=out, out_dtype=out_dtype, p_scale=p_scale,
-                       q_descale=q_descale, k_descale=k_descale, v_descale=v_descale)
+                       q_descale=q_descale, k_descale=k_descale, v_descale=v_descale, normalizer=normalizer,
+                       key_scale=key_scale)
     if check:
         raise_if_bad(bad, q.shape[2], q.shape[1])
     return o

@@ -1,10 +1,11 @@
 """Normaliser triples and the degenerate-denominator error -- the math contract
 of the hot path, mirroring ``ncstream.normalizers`` (normalizers.py:29-126).
 
-Only SPHERICAL (a1=id, a2=square, b=sqrt; normalizers.py:94-100) runs on the
-FlashSign kernel.  SOFTMAX and SIGNED_L1 exist so that reference callers can
-name them; the GPU streamed path rejects them with ``ConfigError`` (no CPU
-fallback).  The scalar maps are kept so ``NormalizerSpec`` objects behave like
+SPHERICAL (a1=id, a2=square, b=sqrt; normalizers.py:94-100) and SIGNED_L1
+(a1=id, a2=abs, b=id; normalizers.py:111-117) run on the FlashSign kernel (the
+epilogue math is a compile-time switch).  SOFTMAX exists so that reference
+callers can name it; the GPU streamed path rejects it with ``ConfigError`` (it
+is not an exp-free FlashSign triple, and there is no CPU fallback).  The scalar maps are kept so ``NormalizerSpec`` objects behave like
 the reference's (e.g. for callers that evaluate ``spec.a2`` themselves).
 """
 

@@ -68,16 +68,20 @@ def piece_views(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tens
             o[b, :, pc.g0 * r: pc.g1 * r])
 
 
-def fwd_shard(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, lo: int, hi: int, fwd, **kw):
+def fwd_shard(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, lo: int, hi: int, fwd,
+              key_scale: torch.Tensor | None = None, **kw):
     """Run ``fwd(q_view, k_view, v_view, out=o_view, **kw)`` over units [lo, hi).
 
     ``q/k/v/o`` are BSHD tensors on this rank's device (``lo/hi`` are unit
-    indices relative to them).  Returns the bad-key tensors ``fwd`` produced
-    (async; nothing synchronises here).
+    indices relative to them); ``key_scale`` [B, Nkv] (optional per-key
+    multiplicities) is sliced by batch row with each piece.  Returns the
+    bad-key tensors ``fwd`` produced (async; nothing synchronises here).
     """
     flags = []
     for pc in pieces(q.shape[0], k.shape[2], lo, hi):
         qv, kv_, vv, ov = piece_views(q, k, v, o, pc)
+        if key_scale is not None:
+            kw["key_scale"] = key_scale[pc.b0: pc.b1]
         res = fwd(qv, kv_, vv, out=ov, **kw)
         if isinstance(res, tuple):
             flags.append(res[1])

@@ -29,8 +29,9 @@ class HostPipeline:
         self.s_cmp = torch.cuda.Stream(self.device)
         self.s_out = torch.cuda.Stream(self.device)
 
-    def _alloc(self, q, k, out):
-        key = (tuple(q.shape[1:]), tuple(k.shape[1:]), q.dtype, out.dtype, self.chunk)
+    def _alloc(self, q, k, out, key_scale=None):
+        key = (tuple(q.shape[1:]), tuple(k.shape[1:]), q.dtype, out.dtype, self.chunk,
+               None if key_scale is None else tuple(key_scale.shape[1:]))
         if key == self._shape_key:
             return
         c = self.chunk
@@ -40,14 +41,19 @@ class HostPipeline:
         self.dv = [torch.empty((c,) + tuple(k.shape[1:]), dtype=k.dtype, device=dev) for _ in range(2)]
         self.do = [torch.empty((c,) + tuple(out.shape[1:]), dtype=out.dtype, device=dev) for _ in range(2)]
         self.bad = [torch.empty(1, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.dm = None if key_scale is None else [
+            torch.empty((c,) + tuple(key_scale.shape[1:]), dtype=torch.float32, device=dev) for _ in range(2)]
         self._shape_key = key
 
     def run(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor, *, scale: float = 1.0,
-            eps: float = 0.0, check: bool = True, **kw) -> torch.Tensor:
-        """O = FlashSign(q, k, v) for host tensors; returns ``out`` (host) after synchronising."""
-        if q.is_cuda or k.is_cuda or v.is_cuda or out.is_cuda:
+            eps: float = 0.0, check: bool = True, key_scale: torch.Tensor | None = None, **kw) -> torch.Tensor:
+        """O = FlashSign(q, k, v) for host tensors; returns ``out`` (host) after synchronising.
+        ``key_scale``: optional host float32 [B, Nkv] key multiplicities (validated when ``check``)."""
+        if q.is_cuda or k.is_cuda or v.is_cuda or out.is_cuda or (key_scale is not None and key_scale.is_cuda):
             raise ValueError("fwd_host expects host (CPU) tensors; use flashsign.fwd for device tensors")
-        self._alloc(q, k, out)
+        if check and key_scale is not None:
+            flashsign.check_key_scale(key_scale)
+        self._alloc(q, k, out, key_scale)
         c = self.chunk
         nb = q.shape[0]
         ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -65,12 +71,15 @@ class HostPipeline:
                     self.dq[s][:n].copy_(q[b0:b1], non_blocking=True)
                     self.dk[s][:n].copy_(k[b0:b1], non_blocking=True)
                     self.dv[s][:n].copy_(v[b0:b1], non_blocking=True)
+                    if key_scale is not None:
+                        self.dm[s][:n].copy_(key_scale[b0:b1], non_blocking=True)
                     ev_in[s].record(self.s_in)
                 with torch.cuda.stream(self.s_cmp):
                     self.s_cmp.wait_event(ev_in[s])
                     _, bad = flashsign.fwd_async(self.dq[s][:n], self.dk[s][:n], self.dv[s][:n], scale=scale,
                                                  eps=eps, out=self.do[s][:n], bad_key=self.bad[s],
-                                                 stream=self.s_cmp, **kw)
+                                                 stream=self.s_cmp,
+                                                 key_scale=None if key_scale is None else self.dm[s][:n], **kw)
                     if check:
                         bad_hits.append((b0, bad.clone()))
                     ev_cmp[s].record(self.s_cmp)

@@ -22,11 +22,12 @@ sys.path.insert(0, REF)
 
 from ncstream.attention import (  # noqa: E402
     TileConfig,
+    apply_multiplicity_array,
     multi_head_attention_array,
     naive_attention_array,
     streamed_attention_array,
 )
-from ncstream.normalizers import SPHERICAL, DegenerateDenominatorError  # noqa: E402
+from ncstream.normalizers import SIGNED_L1, SPHERICAL, DegenerateDenominatorError  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
 
@@ -149,6 +150,57 @@ def main():
             g[f"{name}/err_z"] = np.float64(e.z)
             g[f"{name}/scale"] = np.float64(1.0)
             g[f"{name}/eps"] = np.float64(0.0)
+
+    # ---- SIGNED_L1 (normalizers.py:111-117): the other exp-free triple the kernel compiles
+    q = np.array([[1.0]]); k = np.array([[3.0], [4.0]]); v = np.array([[10.0], [20.0]])
+    put("l1_kat_hand", q, k, v, naive_attention_array(q, k, v, SIGNED_L1, 1.0),
+        extra={"streamed_1_1": streamed_attention_array(q, k, v, SIGNED_L1, 1.0, TileConfig(1, 1))})
+    rng = np.random.default_rng(31)
+    for (y, x, kd) in [(2, 3, 4), (16, 16, 8), (33, 97, 4)]:
+        q, kk, v = rand_qkv(rng, y, x, kd)
+        put(f"l1_grid64_{y}_{x}_{kd}", q, kk, v, naive_attention_array(q, kk, v, SIGNED_L1, 1.0),
+            extra={"streamed_13_7": streamed_attention_array(q, kk, v, SIGNED_L1, 1.0, TileConfig(13, 7))})
+    rng = np.random.default_rng(32)
+    for (y, x, kd) in [(16, 33, 8), (64, 64, 16), (100, 301, 64)]:
+        q, kk, v = rand_qkv(rng, y, x, kd, np.float32)
+        put(f"l1_grid32_{y}_{x}_{kd}", q, kk, v, naive_attention_array(q, kk, v, SIGNED_L1, 1.0),
+            extra={"streamed_5_9": streamed_attention_array(q, kk, v, SIGNED_L1, 1.0, TileConfig(5, 9))})
+    rng = np.random.default_rng(33)
+    q, kk, v = rand_qkv(rng, 40, 70, 64, np.float32)
+    put("l1_scale_eps", q, kk, v, streamed_attention_array(q, kk, v, SIGNED_L1.with_epsilon(1e-3), -0.7,
+                                                           TileConfig()), scale=-0.7, eps=1e-3)
+    rng = np.random.default_rng(34)
+    q = rng.standard_normal((200, 4, 64)).astype(np.float32)
+    k3 = rng.standard_normal((200, 2, 64)).astype(np.float32)
+    v3 = rng.standard_normal((200, 2, 64)).astype(np.float32)
+    put("l1_gqa_4_2_f32", q, k3, v3, multi_head_attention_array(q, k3, v3, SIGNED_L1, h=4, h_kv=2),
+        extra={"h": 4, "h_kv": 2})
+
+    # ---- GRN caller: multiplicity-scaled keys (grn.py:146-173): the fixture keeps the UNSCALED keys
+    # and m; out = multi_head_attention_array(q, apply_multiplicity_array(k, m), v, ...)
+    for tag, spec, seed in (("sph", SPHERICAL, 35), ("l1", SIGNED_L1, 36)):
+        rng = np.random.default_rng(seed)
+        q = rng.standard_normal((200, 4, 64)).astype(np.float32)
+        k3 = rng.standard_normal((200, 2, 64)).astype(np.float32)
+        v3 = rng.standard_normal((200, 2, 64)).astype(np.float32)
+        m = rng.integers(0, 6, 200).astype(np.float64)
+        spec_e = spec.with_epsilon(1e-6)
+        put(f"mult_{tag}_gqa_f32", q, k3, v3,
+            multi_head_attention_array(q, apply_multiplicity_array(k3, m), v3, spec_e, h=4, h_kv=2, scale=1.0),
+            eps=1e-6, extra={"h": 4, "h_kv": 2, "m": m})
+
+    # SIGNED_L1 degenerate row: test_attention.py:69-77 with the L1 triple
+    q = np.array([[1.0, 0.0], [0.0, 0.0]]); k = np.random.default_rng(1).standard_normal((3, 2)); v = np.ones((3, 2))
+    try:
+        streamed_attention_array(q, k, v, SIGNED_L1, 1.0, TileConfig())
+        raise SystemExit("l1_degen_row1: expected DegenerateDenominatorError")
+    except DegenerateDenominatorError as e:
+        cases.append("l1_degen_row1")
+        g["l1_degen_row1/q"], g["l1_degen_row1/k"], g["l1_degen_row1/v"] = q, k, v
+        g["l1_degen_row1/err_row"] = np.int64(int(str(e).rsplit("row ", 1)[1].rstrip(")")))
+        g["l1_degen_row1/err_z"] = np.float64(e.z)
+        g["l1_degen_row1/scale"] = np.float64(1.0)
+        g["l1_degen_row1/eps"] = np.float64(0.0)
 
     g["__cases__"] = np.array(cases)
     np.savez_compressed(OUT, **g)

@@ -89,6 +89,10 @@ def _params(**kw):
     (dict(p_scale=0.0), _lib.FS_ERR_CONFIG, "positive"),
     (dict(heads_q=0), _lib.FS_ERR_SHAPE, "extents"),
     (dict(q=(1 << 20) + 8), _lib.FS_ERR_UNSUPPORTED, "aligned"),
+    (dict(normalizer=7), _lib.FS_ERR_CONFIG, "normalizer"),
+    (dict(key_scale=(1 << 20) + 4), _lib.FS_ERR_UNSUPPORTED, "key_scale must be 16-byte aligned"),
+    (dict(batch=2, key_scale=1 << 20, key_scale_stride=130), _lib.FS_ERR_UNSUPPORTED, "key_scale_stride"),
+    (dict(batch=2, key_scale=1 << 20, key_scale_stride=64), _lib.FS_ERR_UNSUPPORTED, "key_scale_stride"),
 ])
 def test_fs_fwd_validation(kw, status, needle):
     lib = _lib.load()
@@ -150,11 +154,26 @@ def test_compat_config_errors_match_reference():
         streamed_attention(q, q, q, AttentionConfig(SPHERICAL, f16_emulation=True))
 
 
-def test_compat_non_spherical_rejected_on_streamed_path():
-    for spec in (SOFTMAX, SIGNED_L1):
-        with pytest.raises(ConfigError, match="spherical"):
-            streamed_attention_array(np.ones((2, 8), np.float32), np.ones((2, 8), np.float32),
-                                     np.ones((2, 8), np.float32), spec, 1.0, TileConfig())
+def test_compat_softmax_rejected_on_streamed_path():
+    # softmax is not an exp-free FlashSign triple: ConfigError before any device work (no CPU fallback)
+    with pytest.raises(ConfigError, match="exp-free"):
+        streamed_attention_array(np.ones((2, 8), np.float32), np.ones((2, 8), np.float32),
+                                 np.ones((2, 8), np.float32), SOFTMAX, 1.0, TileConfig())
+
+
+def test_multiplicity_validation_matches_reference():
+    # attention.py:381-388: length mismatch -> ShapeMismatchError, negative/non-finite -> ValueError,
+    # raised before any device work
+    from paper_2505_09326_b200.attention import multiplicity_attention_array
+    q = np.ones((4, 2, 8), np.float32)
+    k = np.ones((4, 1, 8), np.float32)
+    with pytest.raises(ShapeMismatchError, match="multiplicity length"):
+        multiplicity_attention_array(q, k, k, np.ones(3), SPHERICAL, 2, 1)
+    for bad in ([1, -1, 0, 2], [1, np.nan, 0, 2], [1, np.inf, 0, 2]):
+        with pytest.raises(ValueError, match="finite and nonnegative"):
+            multiplicity_attention_array(q, k, k, np.array(bad, float), SPHERICAL, 2, 1)
+    with pytest.raises(ConfigError, match="exp-free"):
+        multiplicity_attention_array(q, k, k, np.ones(4), SOFTMAX, 2, 1)
 
 
 def test_default_scales_match_reference():

@@ -443,3 +443,147 @@ def test_host_pipeline_equals_device_path():
     for chunk in (1, 2):
         HostPipeline(0, chunk=chunk).run(qh, kh, vh, oh)
         assert torch.equal(oh, ref.cpu())
+
+
+# ------------------------------------------------------------------ SIGNED_L1 and fused key multiplicities
+
+# signed_l1 outputs are weighted means (weights |s|/sum|s|), so they are O(1/sqrt(N)) and the
+# tolerance is relative: rel-Frobenius and max-abs relative to max|O_ref|.
+TOL_REL = {torch.float16: 3e-3, torch.bfloat16: 1.5e-2, torch.float8_e4m3fn: 8e-2}
+
+
+def check_rel(got, ref, dtype, tag=""):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert np.isfinite(got).all(), f"{tag}: non-finite output"
+    rel_fro = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
+    rel_max = float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+    assert rel_fro <= TOL_REL[dtype] and rel_max <= 4 * TOL_REL[dtype], f"{tag}: rel_fro={rel_fro} rel_max={rel_max}"
+    return rel_fro
+
+
+def exact_of(q, k, v, scale=1.0, eps=0.0, norm="spherical", m=None):
+    from oracle.spherical import exact_batched
+    return exact_batched(q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy(), scale, eps,
+                         norm, None if m is None else m.double().cpu().numpy())
+
+
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16, torch.float8_e4m3fn])
+@pytest.mark.parametrize("shape", [(2, 300, 517, 4, 2, 128), (1, 129, 255, 2, 2, 64), (1, 256, 256, 1, 1, 64)])
+def test_signed_l1_matches_oracle(dt, shape):
+    b, nq, nkv, h, hkv, d = shape
+    if dt == torch.float8_e4m3fn and d != 128:
+        d = 128
+    q = rand_bshd(b, nq, h, d, dt, 50)
+    k = rand_bshd(b, nkv, hkv, d, dt, 51)
+    v = rand_bshd(b, nkv, hkv, d, dt, 52)
+    for scale, eps in ((1.0, 0.0), (-0.7, 1e-3)):
+        o = fs().fwd(q, k, v, scale=scale, eps=eps, out_dtype=torch.float32, normalizer="signed_l1")
+        check_rel(o.cpu().numpy(), exact_of(q, k, v, scale, eps, "signed_l1"), dt, f"l1 {shape} {dt} {scale}")
+
+
+def test_signed_l1_kat_and_degenerate_row():
+    # (3*10 + 4*20) / (3 + 4): exact inputs, fp32 output within one rounding of 110/7
+    q = torch.zeros((1, 1, 1, 64), device="cuda", dtype=torch.bfloat16)
+    k = torch.zeros((1, 2, 1, 64), device="cuda", dtype=torch.bfloat16)
+    v = torch.zeros((1, 2, 1, 64), device="cuda", dtype=torch.bfloat16)
+    q[0, 0, 0, 0] = 1
+    k[0, 0, 0, 0], k[0, 1, 0, 0] = 3, 4
+    v[0, 0, 0, 0], v[0, 1, 0, 0] = 10, 20
+    o = fs().fwd(q, k, v, out_dtype=torch.float32, normalizer="signed_l1")
+    assert abs(float(o[0, 0, 0, 0]) - 110.0 / 7.0) <= 2e-6
+    q2 = rand_bshd(1, 50, 2, 64, torch.bfloat16, 53)
+    k2 = rand_bshd(1, 60, 2, 64, torch.bfloat16, 54)
+    q2[0, 17, 1] = 0
+    _, bad = fs().fwd_async(q2, k2, k2, normalizer="signed_l1")
+    assert fs().decode_bad_key(int(bad.item()), 2, 50) == (0, 1, 17, 0.0)
+
+
+def test_unknown_normalizer_rejected():
+    from paper_2505_09326_b200._errors import ConfigError
+    q = rand_bshd(1, 8, 1, 64, torch.bfloat16, 55)
+    with pytest.raises(ConfigError, match="normalizer"):
+        fs().fwd(q, q, q, normalizer="softmax")
+
+
+@pytest.mark.parametrize("norm", ["spherical", "signed_l1"])
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16, torch.float8_e4m3fn])
+def test_key_scale_matches_oracle(norm, dt):
+    # fused K' = m K (attention.py:381-388, grn.py:150): integer multiplicities 0..5 as in the GRN demo
+    b, nq, nkv, h, hkv, d = 2, 300, 517, 4, 2, (128 if dt == torch.float8_e4m3fn else 64)
+    q = rand_bshd(b, nq, h, d, dt, 60)
+    k = rand_bshd(b, nkv, hkv, d, dt, 61)
+    v = rand_bshd(b, nkv, hkv, d, dt, 62)
+    g = torch.Generator(device="cuda").manual_seed(63)
+    m = torch.randint(0, 6, (b, nkv), generator=g, device="cuda").float()
+    o = fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, normalizer=norm, key_scale=m)
+    ref = exact_of(q, k, v, 1.0, 1e-6, norm, m)
+    if norm == "spherical":
+        check_tol(o.cpu().numpy(), ref, dt, f"ks {norm} {dt}")
+    else:
+        check_rel(o.cpu().numpy(), ref, dt, f"ks {norm} {dt}")
+
+
+def test_key_scale_power_of_two_is_bitwise_prescaled_keys():
+    # m_j * (q . k_j) in fp32 == q . (m_j k_j) when m_j is a power of two (both exact)
+    q = rand_bshd(2, 200, 2, 128, torch.bfloat16, 64)
+    k = rand_bshd(2, 333, 2, 128, torch.bfloat16, 65)
+    v = rand_bshd(2, 333, 2, 128, torch.bfloat16, 66)
+    g = torch.Generator(device="cuda").manual_seed(67)
+    m = torch.tensor([0.0, 0.5, 1.0, 2.0, 4.0], device="cuda")[torch.randint(0, 5, (2, 333), generator=g,
+                                                                            device="cuda")]
+    fused = fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, key_scale=m)
+    pre = fs().fwd(q, (k.float() * m[:, :, None, None]).to(k.dtype), v, eps=1e-6, out_dtype=torch.float32)
+    assert torch.equal(fused, pre)
+    # a strided / unaligned multiplicity view is repacked, same result
+    big = torch.zeros((2, 340), device="cuda")
+    big[:, 1:334] = m
+    assert torch.equal(fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, key_scale=big[:, 1:334]), fused)
+
+
+def test_key_scale_validation():
+    q = rand_bshd(1, 8, 1, 64, torch.bfloat16, 68)
+    from paper_2505_09326_b200.tensor import ShapeMismatchError
+    with pytest.raises(ValueError, match="finite and nonnegative"):
+        fs().fwd(q, q, q, key_scale=torch.tensor([[1.0, -1.0] + [1.0] * 6], device="cuda"))
+    with pytest.raises(ShapeMismatchError, match="key_scale"):
+        fs().fwd(q, q, q, key_scale=torch.ones((1, 7), device="cuda"))
+
+
+@pytest.mark.parametrize("compute", ["fp16", "bf16"])
+def test_compat_signed_l1_against_reference_golden(golden, compute):
+    from paper_2505_09326_b200 import SIGNED_L1
+    at = compat()
+    at.set_compute_dtype(compute)
+    tdt = torch.float16 if compute == "fp16" else torch.bfloat16
+    try:
+        for c in [c for c in golden["__cases__"].tolist() if c.startswith(("l1_grid", "l1_scale_eps", "l1_kat"))]:
+            q, k, v = golden[f"{c}/q"], golden[f"{c}/k"], golden[f"{c}/v"]
+            s, e = float(golden[f"{c}/scale"]), float(golden[f"{c}/eps"])
+            got = at.streamed_attention_array(q, k, v, SIGNED_L1.with_epsilon(e), s, at.TileConfig(13, 7))
+            assert got.dtype == q.dtype
+            check_rel(got, golden[f"{c}/out"], tdt, c)
+        c = "l1_gqa_4_2_f32"
+        got = at.multi_head_attention_array(golden[f"{c}/q"], golden[f"{c}/k"], golden[f"{c}/v"], SIGNED_L1, 4, 2)
+        check_rel(got, golden[f"{c}/out"], tdt, c)
+        with pytest.raises(__import__("paper_2505_09326_b200").DegenerateDenominatorError, match="row 1"):
+            at.streamed_attention_array(golden["l1_degen_row1/q"], golden["l1_degen_row1/k"],
+                                        golden["l1_degen_row1/v"], SIGNED_L1, 1.0, at.TileConfig())
+    finally:
+        at.set_compute_dtype("fp16")
+
+
+@pytest.mark.parametrize("tag", ["sph", "l1"])
+def test_compat_fused_multiplicity_against_reference_golden(golden, tag):
+    # the GRN caller's multi_head_attention_array(q, apply_multiplicity_array(k, m), v, ...) in one launch
+    from paper_2505_09326_b200 import SIGNED_L1, SPHERICAL
+    at = compat()
+    c = f"mult_{tag}_gqa_f32"
+    spec = (SPHERICAL if tag == "sph" else SIGNED_L1).with_epsilon(float(golden[f"{c}/eps"]))
+    got = at.multiplicity_attention_array(golden[f"{c}/q"], golden[f"{c}/k"], golden[f"{c}/v"], golden[f"{c}/m"],
+                                          spec, 4, 2, scale=1.0)
+    want = golden[f"{c}/out"]
+    if tag == "sph":
+        assert np.abs(got.astype(np.float64) - want).max() <= 8e-3 * max(1.0, float(np.abs(want).max()))
+    else:
+        check_rel(got, want, torch.float16, c)

@@ -6,6 +6,7 @@ import pytest
 
 from oracle.spherical import (
     OracleDegenerate,
+    exact_batched,
     gram_batched,
     gram_spherical,
     multi_head_spherical,
@@ -138,3 +139,63 @@ def test_oracle_port_bitwise_equals_live_reference():
     f = rng.standard_normal((64, 16)).astype(np.float32)
     assert np.array_equal(streamed_spherical(f, f, f, 1.0, 0.0, 16, 16, f16=True),
                           streamed_attention_array(f, f, f, SPHERICAL, 1.0, TileConfig(16, 16), f16=True))
+
+
+# ---------------------------------------------------------------- SIGNED_L1 and fused multiplicities
+
+def test_l1_kat_hand_exact(golden):
+    # signed_l1 on the hand KAT: (3*10 + 4*20) / (3 + 4) = 110/7 (normalizers.py:111-117)
+    q, k, v, s, e = _args(golden, "l1_kat_hand")
+    assert golden["l1_kat_hand/out"][0, 0] == 110.0 / 7.0
+    assert naive_spherical(q, k, v, s, e, norm="signed_l1")[0, 0] == 110.0 / 7.0
+    assert streamed_spherical(q, k, v, s, e, 1, 1, norm="signed_l1").tolist() == golden["l1_kat_hand/streamed_1_1"].tolist()
+
+
+@pytest.mark.parametrize("prefix", ["l1_grid64", "l1_grid32", "l1_scale_eps"])
+def test_l1_streamed_and_naive_match_reference(golden, prefix):
+    cases = [c for c in golden["__cases__"].tolist() if c.startswith(prefix)]
+    assert cases
+    for c in cases:
+        q, k, v, s, e = _args(golden, c)
+        want = golden[f"{c}/out"]
+        f32 = q.dtype == np.float32
+        rtol, atol = (1e-5, 1e-6) if f32 else (1e-12, 1e-14)
+        np.testing.assert_allclose(naive_spherical(q, k, v, s, e, norm="signed_l1"), want, rtol=rtol, atol=atol)
+        np.testing.assert_allclose(streamed_spherical(q, k, v, s, e, norm="signed_l1"), want, rtol=rtol, atol=atol)
+        for key, tile in (("streamed_13_7", (13, 7)), ("streamed_5_9", (5, 9))):
+            if f"{c}/{key}" in golden:
+                got = streamed_spherical(q, k, v, s, e, *tile, norm="signed_l1")
+                np.testing.assert_allclose(got, golden[f"{c}/{key}"], rtol=rtol, atol=atol)
+        ex = exact_batched(q[None, :, None], k[None, :, None], v[None, :, None], s, e, norm="signed_l1")[0, :, 0]
+        np.testing.assert_allclose(ex, want, rtol=1e-4 if f32 else 1e-10, atol=1e-5 if f32 else 1e-12)
+
+
+def test_l1_gqa_matches_reference(golden):
+    c = "l1_gqa_4_2_f32"
+    q, k, v, s, e = _args(golden, c)
+    want = golden[f"{c}/out"]
+    np.testing.assert_allclose(multi_head_spherical(q, k, v, 4, 2, s, e, norm="signed_l1"), want, rtol=1e-5, atol=1e-6)
+    got = exact_batched(q[None], k[None], v[None], s, e, norm="signed_l1")[0]
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("tag,norm", [("sph", "spherical"), ("l1", "signed_l1")])
+def test_fused_multiplicity_oracle_matches_reference(golden, tag, norm):
+    # grn.py:150 + 171-173: multi_head_attention_array(q, apply_multiplicity_array(k, m), v, ...)
+    c = f"mult_{tag}_gqa_f32"
+    q, k, v, s, e = _args(golden, c)
+    m = golden[f"{c}/m"]
+    want = golden[f"{c}/out"]
+    got = exact_batched(q[None], k[None], v[None], s, e, norm=norm, m=m[None])[0]
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
+    km = k * m.astype(np.float32)[:, None, None]
+    np.testing.assert_allclose(multi_head_spherical(q, km, v, 4, 2, s, e, norm=norm), want, rtol=1e-5, atol=1e-6)
+
+
+def test_l1_degenerate_row_matches_reference(golden):
+    c = "l1_degen_row1"
+    q, k, v = golden[f"{c}/q"], golden[f"{c}/k"], golden[f"{c}/v"]
+    for fn in (lambda: naive_spherical(q, k, v, norm="signed_l1"), lambda: streamed_spherical(q, k, v, norm="signed_l1")):
+        with pytest.raises(OracleDegenerate) as ei:
+            fn()
+        assert ei.value.row == int(golden[f"{c}/err_row"]) and ei.value.z == float(golden[f"{c}/err_z"])
