@@ -66,21 +66,6 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_NWT
 #define FS_NWT 8  // norm warps per Q tile: 8 (one per lane quarter x column half) or 4
 #endif
-#ifndef FS_NSB3
-#define FS_NSB3 0  // experiment: three rotating S buffers when TMEM allows (d=64); slower so far
-#endif
-#ifndef FS_NOB2
-#define FS_NOB2 1  // experiment knob: allow double-buffered O
-#endif
-#ifndef FS_COLO
-#define FS_COLO 0  // experiment knob: first O column (0 = right after the S buffers)
-#endif
-#ifndef FS_SEQ
-#define FS_SEQ 0  // experiment knob: use the global-sequence issuer with two S buffers too
-#endif
-#ifndef FS_LAG
-#define FS_LAG 2  // rotating-S pipeline: PV(u - FS_LAG) follows QK(u)
-#endif
 #ifndef FS_STAGES16
 #define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=64 16-bit, d=128 e4m3)
 #endif
@@ -146,11 +131,11 @@ struct Cfg {
   static constexpr int RING_OFF = NQT * NQB * Q_TILE_BYTES;
   static constexpr int BAR_OFF = RING_OFF + STAGES * SLOT_BYTES;
   static constexpr int ZBUF_OFF = BAR_OFF + 512;
-  // S buffers in TMEM.  Three when they fit next to the O accumulators (d=64): S allocations
-  // rotate over them, so each norm warp gets a four-MMA window instead of two.
-  static constexpr int NSB = (FS_NSB3 && 3 * BN + NQT * D <= TMEM_COLS) ? 3 : 2;
+  // S buffers in TMEM: one per Q tile (P aliases its S).  (A third rotating buffer at d=64, for
+  // a four-MMA norm window, measured slower with a generic issuer; see profiles/r1/SUMMARY.md.)
+  static constexpr int NSB = 2;
   // O accumulators double-buffered in TMEM when they still fit: the epilogue never gates the MMAs.
-  static constexpr int NOB = (FS_NOB2 && NSB * BN + 2 * NQT * D <= TMEM_COLS) ? 2 : 1;
+  static constexpr int NOB = (NSB * BN + 2 * NQT * D <= TMEM_COLS) ? 2 : 1;
   // per-key multiplicities m_j of each V slot's keys (fused K' = m K, grn.py:150)
   static constexpr int MS_OFF = ZBUF_OFF + NQT * NOB * 2 * BM * 4;
   static constexpr int MS_SLOT_BYTES = BN * 4;
@@ -158,9 +143,8 @@ struct Cfg {
   static constexpr int QK_STEPS = ROW_BYTES / 32;                          // 32 B of K-dim per MMA
   static constexpr int PV_STEPS = BN / TR::KSTEP;
   static constexpr uint32_t COL_S0 = 0;
-  static constexpr uint32_t COL_O0 = FS_COLO ? FS_COLO : NSB * BN;
+  static constexpr uint32_t COL_O0 = NSB * BN;
   static_assert(NSB * BN + NOB * NQT * D <= TMEM_COLS, "TMEM budget");
-  static_assert(NSB == 2 || NQB == 2, "the rotating-S pipeline issues the next work tile's QK early");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(PV_STEPS % 2 == 0, "PV is issued in two K-halves");
   static constexpr uint32_t IDESC_QK = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, BM, BN);
@@ -170,8 +154,8 @@ struct Cfg {
 struct Bars {
   uint64_t q_full[NQT][2], q_empty[NQT][2];
   uint64_t kv_full[8], kv_empty[8];
-  uint64_t s_full[3];       // per S buffer
-  uint64_t p_full[3][2];    // per S buffer and half of the P tile
+  uint64_t s_full[2];       // per S buffer (= Q tile)
+  uint64_t p_full[2][2];    // per S buffer and half of the P tile
   uint64_t o_full[NQT][2], o_empty[NQT][2];
   uint64_t z_full[NQT][2], z_empty[NQT][2];
   uint32_t tmem_base;
@@ -269,7 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 32) {
 #pragma unroll
-    for (int b = 0; b < 3; ++b) {
+    for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&bars->s_full[b], 1);
       ptx::mbar_init(&bars->p_full[b][0], 4);
       ptx::mbar_init(&bars->p_full[b][1], 4);
@@ -311,13 +295,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol_q = ptx::policy_evict_first();
       const uint64_t pol_kv = ptx::policy_evict_last();
       uint32_t kv_i = 0;  // loads issued into the ring so far (K and V alternate)
-      int it = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
-        const TileCoord tc = decode_tile(tile, p);
-        const int head_kv = static_cast<int>((static_cast<int64_t>(tc.head) * p.heads_kv) / p.heads_q);
-        const int q_row0 = tc.qblk * (NQT * BM);
-        const int qb = it % C::NQB;
-        const uint32_t q_use = static_cast<uint32_t>(it / C::NQB);
+      // Q tiles of work tile `tile_` (the it_-th of this CTA) into buffer it_ % NQB once it is free
+      auto load_q = [&](int tile_, int it_) {
+        const TileCoord qc = decode_tile(tile_, p);
+        const int qb = it_ % C::NQB;
+        const uint32_t q_use = static_cast<uint32_t>(it_ / C::NQB);
 #pragma unroll
         for (int t = 0; t < NQT; ++t) {
           ptx::mbar_wait(&bars->q_empty[t][qb], (q_use & 1u) ^ 1u);
@@ -325,17 +307,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int db = 0; db < C::NDB; ++db)
             ptx::tma_load_4d(smem + (t * C::NQB + qb) * C::Q_TILE_BYTES + db * (BM * 128), &tm_q,
-                             &bars->q_full[t][qb], db * C::BOXW, q_row0 + t * BM, tc.head, tc.batch, pol_q);
+                             &bars->q_full[t][qb], db * C::BOXW, qc.qblk * (NQT * BM) + t * BM, qc.head,
+                             qc.batch, pol_q);
         }
-        if (C::NQB == 1 && tile + static_cast<int>(gridDim.x) < p.n_tiles) {
+      };
+      load_q(blockIdx.x, 0);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+        const TileCoord tc = decode_tile(tile, p);
+        const int head_kv = static_cast<int>((static_cast<int64_t>(tc.head) * p.heads_kv) / p.heads_q);
+        const int next = tile + static_cast<int>(gridDim.x);
+        if (C::NQB == 1 && next < p.n_tiles) {
           // single Q buffer: pull the next work tile's Q into L2 now so its reload is an L2 hit
-          const TileCoord nx = decode_tile(tile + gridDim.x, p);
+          const TileCoord nx = decode_tile(next, p);
 #pragma unroll
           for (int t = 0; t < NQT; ++t)
 #pragma unroll
             for (int db = 0; db < C::NDB; ++db)
               ptx::tma_prefetch_l2_4d(&tm_q, db * C::BOXW, nx.qblk * (NQT * BM) + t * BM, nx.head, nx.batch);
         }
+        // double-buffered Q: the next work tile's Q goes out right after this tile's first two
+        // K/V tiles, a whole work tile ahead of its first QK
+        const int q_next_at = C::NQB == 2 ? std::min(3, 2 * n_kv_tiles - 1) : 2 * n_kv_tiles - 1;
         for (int i = 0; i < 2 * n_kv_tiles; ++i, ++kv_i) {
           const uint32_t slot = kv_i % C::STAGES;
           const uint32_t round = kv_i / C::STAGES;
@@ -351,6 +344,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int db = 0; db < C::NDB; ++db)
             ptx::tma_load_4d(smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128), tm, &bars->kv_full[slot],
                              db * C::BOXW, key0, head_kv, tc.batch, pol_kv);
+          if (i == q_next_at && next < p.n_tiles) load_q(next, it + 1);
         }
       }
     }
@@ -365,10 +359,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t k_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, 16, 1024);
       const uint64_t v_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, BN * 128, 1024);
 #if FS_PROF
-      long long pr_pw = 0, pr_pn = 0, pr_kw = 0, pr_kn = 0, pr_vw = 0, pr_ow = 0, pr_qw = 0, pr_qi = 0;
+      long long pr_pw = 0, pr_pn = 0, pr_kw = 0, pr_kn = 0;
       const long long pr_t0 = clock64();
 #endif
-      if constexpr (C::NSB == 2 && !FS_SEQ) {
+      {
       uint32_t kv_i = 0;                 // ring position of this work tile's K_0
       uint32_t p_use[NQT] = {0u, 0u};    // completed phases of p_full[t][*]
       int it = 0;
@@ -475,135 +469,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         kv_i += 2 * n_kv_tiles;
       }
-      } else {
-        // ---- three rotating S buffers (d=64): one global sequence over this CTA's S allocations
-        // u = 2*jg + t (jg = K/V tiles streamed so far, t = Q tile), buffer u % 3, issued as
-        //     QK(u) PV(u-2)   so S(u) has PV(u-2) QK(u+1) PV(u-1) QK(u+2) to become P(u).
-        // The sequence runs across work tiles: the next tile's QKs overlap this tile's last PVs.
-        const uint32_t L = static_cast<uint32_t>(n_kv_tiles);
-        const uint32_t n_my = (p.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-        const uint32_t U = 2u * L * n_my;
-        // position of S allocation u in (work tile, K/V tile, Q tile) order, advanced incrementally
-        struct Cursor {
-          uint32_t t = 0, j = 0, it = 0, jg = 0, sb = 0, sph = 0;
-          __device__ void next(uint32_t L_) {
-            if (++sb == C::NSB) { sb = 0; sph ^= 1u; }
-            if (t == 0) { t = 1; return; }
-            t = 0;
-            ++jg;
-            if (++j == L_) { j = 0; ++it; }
-          }
-        };
-        Cursor cq, cp;  // QK stream and PV stream (two allocations behind)
-        auto qk3 = [&](const Cursor& c) {
-          const uint32_t qb = c.it & (C::NQB - 1), k_idx = 2u * c.jg, k_slot = k_idx % C::STAGES;
-          if (c.t == 0) {
-#if FS_PROF
-            const long long tk0 = clock64();
-#endif
-            ptx::mbar_wait(&bars->kv_full[k_slot], (k_idx / C::STAGES) & 1u);
-#if FS_PROF
-            pr_kw += clock64() - tk0;
-            ++pr_kn;
-#endif
-          }
-#if FS_PROF
-          const long long tq0 = clock64();
-#endif
-          if (c.j == 0) ptx::mbar_wait(&bars->q_full[c.t][qb], (c.it / C::NQB) & 1u);
-          ptx::tc_fence_after();
-#if FS_PROF
-          const long long tq1 = clock64();
-          pr_qw += tq1 - tq0;
-#endif
-          if (leader) {
-            const uint64_t a0 = q_desc + static_cast<uint32_t>(((c.t * C::NQB + qb) * C::Q_TILE_BYTES) >> 4);
-            const uint64_t b0 = k_desc + static_cast<uint32_t>((k_slot * C::SLOT_BYTES) >> 4);
-            const uint32_t d_tmem = tmem + C::COL_S0 + c.sb * BN;
-#pragma unroll
-            for (int ks = 0; ks < C::QK_STEPS; ++ks) {
-              const uint32_t off = ((ks * 32 / 128) * (BM * 128) + (ks * 32) % 128) >> 4;
-              if constexpr (TR::F8)
-                ptx::mma_f8_ss(d_tmem, a0 + off, b0 + off, C::IDESC_QK, ks > 0);
-              else
-                ptx::mma_f16_ss(d_tmem, a0 + off, b0 + off, C::IDESC_QK, ks > 0);
-            }
-            ptx::tc_commit(&bars->s_full[c.sb]);
-            if (c.t == 1) ptx::tc_commit(&bars->kv_empty[k_slot]);
-            if (c.j == L - 1) ptx::tc_commit(&bars->q_empty[c.t][qb]);
-          }
-          __syncwarp();
-#if FS_PROF
-          pr_qi += clock64() - tq1;
-#endif
-        };
-        auto pv3 = [&](const Cursor& c) {
-          const uint32_t ob = c.it % C::NOB, v_idx = 2u * c.jg + 1u, v_slot = v_idx % C::STAGES;
-#if FS_PROF
-          const long long tv0 = clock64();
-#endif
-          if (c.t == 0) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
-#if FS_PROF
-          const long long tv1 = clock64();
-          pr_vw += tv1 - tv0;
-#endif
-          if (c.j == 0) ptx::mbar_wait(&bars->o_empty[c.t][ob], ((c.it / C::NOB) & 1u) ^ 1u);
-#if FS_PROF
-          pr_ow += clock64() - tv1;
-#endif
-          const uint64_t b0 = v_desc + static_cast<uint32_t>((v_slot * C::SLOT_BYTES) >> 4);
-          const uint32_t a_tmem = tmem + C::COL_S0 + c.sb * BN;
-          const uint32_t d_tmem = tmem + C::COL_O0 + (ob * NQT + c.t) * D;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#if FS_PROF
-            const long long tw0 = clock64();
-#endif
-            ptx::mbar_wait(&bars->p_full[c.sb][h], c.sph);
-#if FS_PROF
-            pr_pw += clock64() - tw0;
-            ++pr_pn;
-#endif
-            ptx::tc_fence_after();
-            if (leader) {
-#pragma unroll
-              for (int k2 = 0; k2 < C::PV_STEPS / 2; ++k2) {
-                const int ks = h * (C::PV_STEPS / 2) + k2;
-                const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
-                const uint32_t at = a_tmem + h * (BN / 2) + k2 * (TR::KSTEP * C::EB / 4);
-                const uint32_t acc = (c.j > 0 || ks > 0) ? 1u : 0u;
-                if constexpr (TR::F8)
-                  ptx::mma_f8_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
-                else
-                  ptx::mma_f16_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
-              }
-            }
-            __syncwarp();
-          }
-          if (leader) {
-            if (c.t == 1) ptx::tc_commit(&bars->kv_empty[v_slot]);
-            if (c.j == L - 1) ptx::tc_commit(&bars->o_full[c.t][ob]);
-          }
-          __syncwarp();
-        };
-        for (uint32_t u = 0; u < U; ++u) {
-          qk3(cq);
-          cq.next(L);
-          if (u >= FS_LAG) {
-            pv3(cp);
-            cp.next(L);
-          }
-        }
-#pragma unroll
-        for (int r2 = 0; r2 < FS_LAG; ++r2) {
-          pv3(cp);
-          cp.next(L);
-        }
       }
 #if FS_PROF
       if (leader) { FS_PROF_ADD(2, pr_pw); FS_PROF_ADD(3, pr_pn); FS_PROF_ADD(4, pr_kw); FS_PROF_ADD(5, pr_kn);
-                    FS_PROF_ADD(7, clock64() - pr_t0); FS_PROF_ADD(8, pr_vw); FS_PROF_ADD(9, pr_ow);
-                    FS_PROF_ADD(10, pr_qw); FS_PROF_ADD(11, pr_qi); }
+                    FS_PROF_ADD(7, clock64() - pr_t0); }
 #endif
     }
   } else if (warp >= WARP_NORM0 && warp < WARP_EPI) {
@@ -632,9 +501,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #if FS_PROF
         const long long tn0 = clock64();
 #endif
-        // S allocation u = 2*jg + t lives in buffer u % NSB (see the MMA issuer)
-        const uint32_t u = 2u * s_use + t, sb = u % C::NSB;
-        ptx::mbar_wait(&bars->s_full[sb], (u / C::NSB) & 1u);
+        const uint32_t sb = t;  // S_t's TMEM buffer; one phase per K/V tile
+        ptx::mbar_wait(&bars->s_full[sb], s_use & 1u);
         const uint32_t s_base = s_lane + sb * BN;
         // key multiplicities of this K/V tile ride in V_j's ring slot; that slot is released only
         // after PV_1(j), which needs this warp's P, so they stay valid while they are read here

@@ -123,9 +123,7 @@ def run(cases, rounds):
             b = list(buf)
             prof = {"norm_cyc_per_tile": b[0] / max(b[1], 1), "norm_wait_s_cyc": b[6] / max(b[1], 1),
                     "mma_wait_p_cyc": b[2] / max(b[3], 1), "mma_wait_kv_cyc": b[4] / max(b[5], 1),
-                    "mma_cyc_per_kv_tile": b[7] / max(b[5], 1), "mma_wait_v_per_kv": b[8] / max(b[5], 1),
-                    "mma_wait_o_per_kv": b[9] / max(b[5], 1), "mma_wait_q_per_kv": b[10] / max(b[5], 1),
-                    "mma_qk_issue_per_kv": b[11] / max(b[5], 1)}
+                    "mma_cyc_per_kv_tile": b[7] / max(b[5], 1)}
             res[f"{cname}/{name}/prof"] = prof
             print(cname, name, "prof", {k: round(v, 1) for k, v in prof.items()}, flush=True)
         ref = next(iter(outs.values()))
