@@ -86,7 +86,12 @@ typedef struct {
   uint64_t *bad_key;
   int32_t tile_m_hint, tile_n_hint; /* TileConfig (g_y, s_x); advisory only    */
   int32_t normalizer;               /* fs_normalizer; 0 = SPHERICAL            */
-  int32_t reserved0;                /* must be 0                               */
+  /* Split K/V stream (streaming.py:122-128 merge; Lemma 1): 0 or 1 = one pass.
+     S > 1 cuts every (b, h) K/V stream into S contiguous ranges computed by independent work
+     tiles (for small B*H with long N); partial numerators and z go to `partial` and fs_fwd then
+     runs the combine kernel (O = sum_s num_s / b(sum_s z_s + eps)) on the same stream.
+     fs_kv_splits(p) returns the effective S (clamped so that every range is non-empty). */
+  int32_t kv_splits;
   /* Optional per-key multiplicity m (NULL: none): fp32 device array [batch, seqlen_kv],
      element (b, n) at key_scale[b*key_scale_stride + n], shared by all kv heads -- the
      reference's apply_multiplicity_array(K, m) (attention.py:381-388) fused into the
@@ -94,10 +99,28 @@ typedef struct {
      ValueError).  16-byte aligned; key_scale_stride*4 a multiple of 16 when batch > 1. */
   const float *key_scale;
   int64_t key_scale_stride;
+  /* fp32 workspace of fs_partial_floats(p) floats, 16-byte aligned (needed when the effective
+     kv_splits > 1 or partial_only): numerators [S][B][H][Nq][Dk] then z [S][B][H][Nq],
+     Dk = 128 for e4m3 or head_dim > 64, else 64.  Caller-owned; fs_fwd never allocates. */
+  float *partial;
+  /* 1: stop after writing the partials (no O, no bad-row key).  Context parallelism: every rank
+     runs its K/V shard with partial_only = 1, the ranks all-reduce(sum) `partial`, then each
+     calls fs_combine(p, 1, stream) to normalise. */
+  int32_t partial_only;
+  int32_t reserved1; /* must be 0 */
 } fs_fwd_params;
 
 /* Validate, encode TMA descriptors (cached per call), launch.  Async. */
 fs_status fs_fwd(const fs_fwd_params *p, fs_stream_t stream);
+
+/* Effective number of K/V ranges for p (>= 1) and the partial workspace size in floats. */
+int32_t fs_kv_splits(const fs_fwd_params *p);
+int64_t fs_partial_floats(const fs_fwd_params *p);
+
+/* O = sum_s num_s / b(sum_s z_s + eps) over the first n_parts partials in p->partial, written to
+   p->o with p->o_stride / out_dtype, and the bad-row key (reset first) -- the merge step of the
+   split / context-parallel path.  Async on `stream`. */
+fs_status fs_combine(const fs_fwd_params *p, int32_t n_parts, fs_stream_t stream);
 
 /* Thread-local text of the last non-FS_OK status. */
 const char *fs_last_error(void);

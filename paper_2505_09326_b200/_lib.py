@@ -20,7 +20,8 @@ FS_NORM_SPHERICAL, FS_NORM_SIGNED_L1 = range(2)
 FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
 
 # every symbol include/flashsign.h declares
-EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version")
+EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version", "fs_kv_splits", "fs_partial_floats",
+                    "fs_combine")
 
 
 class FsFwdParams(ctypes.Structure):
@@ -53,9 +54,12 @@ class FsFwdParams(ctypes.Structure):
         ("tile_m_hint", ctypes.c_int32),
         ("tile_n_hint", ctypes.c_int32),
         ("normalizer", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("kv_splits", ctypes.c_int32),
         ("key_scale", ctypes.c_void_p),
         ("key_scale_stride", ctypes.c_int64),
+        ("partial", ctypes.c_void_p),
+        ("partial_only", ctypes.c_int32),
+        ("reserved1", ctypes.c_int32),
     ]
 
 
@@ -85,6 +89,12 @@ def load() -> ctypes.CDLL:
             lib.fs_query_tile.restype = ctypes.c_int
             lib.fs_version.argtypes = []
             lib.fs_version.restype = ctypes.c_int
+            lib.fs_kv_splits.argtypes = [ctypes.POINTER(FsFwdParams)]
+            lib.fs_kv_splits.restype = ctypes.c_int32
+            lib.fs_partial_floats.argtypes = [ctypes.POINTER(FsFwdParams)]
+            lib.fs_partial_floats.restype = ctypes.c_int64
+            lib.fs_combine.argtypes = [ctypes.POINTER(FsFwdParams), ctypes.c_int32, ctypes.c_void_p]
+            lib.fs_combine.restype = ctypes.c_int
             _lib = lib
     return _lib
 

@@ -316,9 +316,7 @@ def naive_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: Nor
     y, x, _ = _check_qkv(q, k, v)
     dev = _device()
     f32 = q.dtype == np.float32
-    qd = torch.from_numpy(np.ascontiguousarray(q, dtype=np.float64)).to(dev)
-    kd = torch.from_numpy(np.ascontiguousarray(k, dtype=np.float64)).to(dev)
-    vd = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
+    qd, kd, vd = (torch.from_numpy(np.array(a, dtype=np.float64, order="C")).to(dev) for a in (q, k, v))
     s = qd @ kd.T
     if f32:
         s = s.float()

@@ -88,6 +88,13 @@ struct KParams {
   float p_scale;
   float ovf_z;      // a P chunk whose sum of a2(s) stays below this cannot overflow (PMAX/|p_scale|)^{2|1}
   uint64_t* bad_key;
+  // split K/V stream (streaming.py:122-128 merge): work tile = (batch, head, split, query block)
+  int32_t n_batch;
+  int32_t kv_splits;       // >= 1
+  int32_t split_tiles;     // K/V tiles per split (the last split may be shorter)
+  int32_t n_kv_tiles;      // ceil(seqlen_kv / BN)
+  float* part_num;         // non-NULL: write fp32 partial numerators [S][B][H][Nq][D] here instead of O
+  float* part_z;           //           and partial z [S][B][H][Nq] (no normalisation, no bad-row check)
 };
 
 template <int IN>
@@ -220,14 +227,18 @@ __device__ __forceinline__ void store32(typename OutT<OUT>::T* dst, const float*
 }
 
 struct TileCoord {
-  int qblk, head, batch;
+  int qblk, head, batch, split, kb0, L;  // K/V tiles [kb0, kb0 + L) of this work tile
 };
 __device__ __forceinline__ TileCoord decode_tile(int tile, const KParams& p) {
   TileCoord c;
   c.qblk = tile % p.n_qblk;
-  const int bh = tile / p.n_qblk;
+  const int rest = tile / p.n_qblk;
+  c.split = rest % p.kv_splits;
+  const int bh = rest / p.kv_splits;
   c.head = bh % p.heads_q;
   c.batch = bh / p.heads_q;
+  c.kb0 = c.split * p.split_tiles;
+  c.L = min(p.split_tiles, p.n_kv_tiles - c.kb0);
   return c;
 }
 
@@ -328,15 +339,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         // double-buffered Q: the next work tile's Q goes out right after this tile's first two
         // K/V tiles, a whole work tile ahead of its first QK
-        const int q_next_at = C::NQB == 2 ? std::min(3, 2 * n_kv_tiles - 1) : 2 * n_kv_tiles - 1;
-        for (int i = 0; i < 2 * n_kv_tiles; ++i, ++kv_i) {
+        const int L = tc.L;
+        const int q_next_at = C::NQB == 2 ? std::min(3, 2 * L - 1) : 2 * L - 1;
+        for (int i = 0; i < 2 * L; ++i, ++kv_i) {
           const uint32_t slot = kv_i % C::STAGES;
           const uint32_t round = kv_i / C::STAGES;
           ptx::mbar_wait(&bars->kv_empty[slot], (round & 1u) ^ 1u);
           const bool with_m = KS && (i & 1);  // V slots also carry the tile's key multiplicities
           ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::SLOT_BYTES + (with_m ? C::MS_SLOT_BYTES : 0));
           const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
-          const int key0 = (i >> 1) * BN;
+          const int key0 = (tc.kb0 + (i >> 1)) * BN;
           if (with_m)
             ptx::tma_load_2d(smem + C::MS_OFF + slot * C::MS_SLOT_BYTES, &tm_m, &bars->kv_full[slot], key0,
                              tc.batch, pol_kv);
@@ -371,6 +383,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t q_use = static_cast<uint32_t>(it / C::NQB);
         const int ob = it % C::NOB;
         const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
+        const int L = decode_tile(tile, p).L;
         auto qk = [&](int t, uint32_t slot) {
           const uint64_t a0 = q_desc + static_cast<uint32_t>(((t * C::NQB + qb) * C::Q_TILE_BYTES) >> 4);
           const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
@@ -423,7 +436,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int t = 0; t < NQT; ++t) ptx::mbar_wait(&bars->q_full[t][qb], q_use & 1u);
         ptx::tc_fence_after();
         uint32_t prev_v_slot = 0;
-        for (int j = 0; j < n_kv_tiles; ++j) {
+        for (int j = 0; j < L; ++j) {
           const uint32_t k_idx = kv_i + 2 * j, v_idx = k_idx + 1;
           const uint32_t k_slot = k_idx % C::STAGES, v_slot = v_idx % C::STAGES;
 #if FS_PROF
@@ -438,7 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (leader) {
             qk(0, k_slot);
             ptx::tc_commit(&bars->s_full[0]);
-            if (j == n_kv_tiles - 1) ptx::tc_commit(&bars->q_empty[0][qb]);
+            if (j == L - 1) ptx::tc_commit(&bars->q_empty[0][qb]);
           }
           __syncwarp();
           if (j > 0) {
@@ -450,24 +463,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             qk(1, k_slot);
             ptx::tc_commit(&bars->s_full[1]);
             ptx::tc_commit(&bars->kv_empty[k_slot]);
-            if (j == n_kv_tiles - 1) ptx::tc_commit(&bars->q_empty[1][qb]);
+            if (j == L - 1) ptx::tc_commit(&bars->q_empty[1][qb]);
           }
           __syncwarp();
           ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
           pv(0, v_slot, j);
-          if (j == n_kv_tiles - 1) {
+          if (j == L - 1) {
             if (leader) ptx::tc_commit(&bars->o_full[0][ob]);
             __syncwarp();
           }
           prev_v_slot = v_slot;
         }
-        pv(1, prev_v_slot, n_kv_tiles - 1);
+        pv(1, prev_v_slot, L - 1);
         if (leader) {
           ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
           ptx::tc_commit(&bars->o_full[1][ob]);
         }
         __syncwarp();
-        kv_i += 2 * n_kv_tiles;
+        kv_i += 2 * L;
       }
       }
 #if FS_PROF
@@ -497,7 +510,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int ob = it % C::NOB;
       float2 za = make_float2(0.f, 0.f), zb = za;
       bool ovf = false;
-      for (int j = 0; j < n_kv_tiles; ++j) {
+      const int L = decode_tile(tile, p).L;
+      for (int j = 0; j < L; ++j) {
 #if FS_PROF
         const long long tn0 = clock64();
 #endif
@@ -628,18 +642,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = 0; t < NQT; ++t) {
         // zr = sum_j a2(c s_ij) (what the reference calls z), or +inf for a P overflow
         float zr = 0.f;
-        if (n_kv_tiles > 0) {
+        if (tc.L > 0) {
           ptx::mbar_wait(&bars->z_full[t][ob], o_use & 1u);
           const float* zt = zbuf + (t * C::NOB + ob) * 2 * BM + r;
           zr = p.zmul * (zt[0] + zt[BM]);  // the two column halves of the row
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&bars->z_empty[t][ob]);
         }
-        const float den = NORM == FS_NORM_SIGNED_L1 ? zr + p.eps : sqrtf(zr + p.eps);
-        const bool bad = !(den > 0.f) || isinf(den);
-        const float mul = __fdiv_rn(p.out_mul, den);
         const int row = tc.qblk * (NQT * BM) + t * BM + r;
         const bool live = row < p.seqlen_q;
+        const bool partial = p.part_num != nullptr;
+        const float den = NORM == FS_NORM_SIGNED_L1 ? zr + p.eps : sqrtf(zr + p.eps);
+        const bool bad = !partial && (!(den > 0.f) || isinf(den));
+        // partial mode: the unnormalised numerator (the combine step divides by b(sum z + eps))
+        const float mul = partial ? p.out_mul : __fdiv_rn(p.out_mul, den);
+        // partial row index: ((split * B + batch) * H + head) * Nq + row
+        const int64_t prow =
+            ((static_cast<int64_t>(tc.split) * p.n_batch + tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
+        if (partial && live) p.part_z[prow] = zr;
         if (live && bad && p.bad_key != nullptr) {
           const uint64_t lin = (static_cast<uint64_t>(tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
           atomicMin(reinterpret_cast<unsigned long long*>(p.bad_key),
@@ -648,7 +668,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         OT* dst = reinterpret_cast<OT*>(p.o) + tc.batch * p.o_sb + static_cast<int64_t>(row) * p.o_sn +
                   tc.head * p.o_sh;
         const uint32_t o_addr = tmem + lane_off + C::COL_O0 + (ob * NQT + t) * D;
-        if (n_kv_tiles > 0) {
+        if (tc.L > 0) {
           ptx::mbar_wait(&bars->o_full[t][ob], o_use & 1u);
           ptx::tc_fence_after();
         }
@@ -656,7 +676,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int c = 0; c < D / 32; ++c) {
           uint32_t acc[32];
           float v[32];
-          if (n_kv_tiles > 0) {
+          if (tc.L > 0) {
             ptx::tmem_ld32(o_addr + c * 32, acc);  // warp-collective: every lane participates
             ptx::tmem_wait_ld();
             if (c == D / 32 - 1) {  // all of O_t is in registers: release the accumulator
@@ -670,7 +690,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(acc[i]) * mul;
-          if (live && c * 32 < p.head_dim) store32<OUT>(dst + c * 32, v, c * 32, p.head_dim);
+          if (partial) {
+            if (live) store32<FS_F32>(p.part_num + prow * D + c * 32, v, c * 32, D);
+          } else if (live && c * 32 < p.head_dim) {
+            store32<OUT>(dst + c * 32, v, c * 32, p.head_dim);
+          }
         }
       }
     }
@@ -768,6 +792,101 @@ static int num_sms() {
   return cache[dev];
 }
 
+// K/V split plan: requested splits clamped to [1, n_kv_tiles], then every split non-empty.
+struct SplitPlan {
+  int32_t splits, split_tiles, n_kv_tiles;
+};
+static SplitPlan split_plan(const fs_fwd_params* p) {
+  SplitPlan sp;
+  sp.n_kv_tiles = (p->seqlen_kv + BN - 1) / BN;
+  int s = std::max(1, p->kv_splits);
+  s = std::max(1, std::min(s, sp.n_kv_tiles));
+  sp.split_tiles = sp.n_kv_tiles > 0 ? (sp.n_kv_tiles + s - 1) / s : 0;
+  sp.splits = sp.split_tiles > 0 ? (sp.n_kv_tiles + sp.split_tiles - 1) / sp.split_tiles : 1;
+  return sp;
+}
+static int kernel_d(const fs_fwd_params* p) { return (p->in_dtype == FS_E4M3 || p->head_dim > 64) ? 128 : 64; }
+
+// Merge of K/V-range partials (streaming.py:122-128, Lemma 1: (o, z) add, no
+// rescale): O = sum_s num_s / b(sum_s z_s + eps), plus the bad-row key.  One thread per 4 columns.
+template <int OUT, int NORM, int DK>
+__global__ void __launch_bounds__(256) flashsign_combine_kernel(const float* __restrict__ num,
+                                                                const float* __restrict__ zp, int n_parts,
+                                                                int64_t rows, int heads, int seqlen_q, void* o,
+                                                                int64_t o_sb, int64_t o_sn, int64_t o_sh,
+                                                                int head_dim, float eps, uint64_t* bad_key) {
+  constexpr int TPR = DK / 4;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = gid / TPR;
+  const int c4 = static_cast<int>(gid % TPR) * 4;
+  if (row >= rows) return;
+  float z = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < n_parts; ++s) {
+    z += zp[s * rows + row];
+    const float4 a = *reinterpret_cast<const float4*>(num + (s * rows + row) * DK + c4);
+    acc.x += a.x;
+    acc.y += a.y;
+    acc.z += a.z;
+    acc.w += a.w;
+  }
+  const float den = NORM == FS_NORM_SIGNED_L1 ? z + eps : sqrtf(z + eps);
+  if ((!(den > 0.f) || isinf(den)) && c4 == 0 && bad_key != nullptr)
+    atomicMin(reinterpret_cast<unsigned long long*>(bad_key),
+              static_cast<unsigned long long>((static_cast<uint64_t>(row) << 32) | __float_as_uint(z)));
+  if (c4 >= head_dim) return;
+  const float inv = __fdiv_rn(1.0f, den);
+  const int n = static_cast<int>(row % seqlen_q);
+  const int64_t bh = row / seqlen_q;
+  const int h = static_cast<int>(bh % heads);
+  const int64_t b = bh / heads;
+  using OT = typename OutT<OUT>::T;
+  OT* dst = reinterpret_cast<OT*>(o) + b * o_sb + static_cast<int64_t>(n) * o_sn + h * o_sh + c4;
+  const float v0 = acc.x * inv, v1 = acc.y * inv, v2 = acc.z * inv, v3 = acc.w * inv;
+  if constexpr (OUT == FS_F32) {
+    *reinterpret_cast<float4*>(dst) = make_float4(v0, v1, v2, v3);
+  } else {
+    uint2 w;
+    w.x = pack2<OUT>(v0, v1);
+    w.y = pack2<OUT>(v2, v3);
+    *reinterpret_cast<uint2*>(dst) = w;
+  }
+}
+
+template <int DK>
+static fs_status combine(const fs_fwd_params* p, int n_parts, cudaStream_t stream) {
+  const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
+  if (rows == 0) return FS_OK;
+  const float* num = p->partial;
+  const float* zp = p->partial + (int64_t)n_parts * rows * DK;
+  const int64_t threads = rows * (DK / 4);
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  auto go = [&](auto kern) {
+    kern<<<blocks, 256, 0, stream>>>(num, zp, n_parts, rows, p->heads_q, p->seqlen_q, p->o, p->o_stride[0],
+                                     p->o_stride[1], p->o_stride[2], p->head_dim, p->eps, p->bad_key);
+  };
+  const bool l1 = p->normalizer == FS_NORM_SIGNED_L1;
+  switch (p->out_dtype) {
+    case FS_F32:
+      l1 ? go(flashsign_combine_kernel<FS_F32, FS_NORM_SIGNED_L1, DK>)
+         : go(flashsign_combine_kernel<FS_F32, FS_NORM_SPHERICAL, DK>);
+      break;
+    case FS_BF16:
+      l1 ? go(flashsign_combine_kernel<FS_BF16, FS_NORM_SIGNED_L1, DK>)
+         : go(flashsign_combine_kernel<FS_BF16, FS_NORM_SPHERICAL, DK>);
+      break;
+    case FS_F16:
+      l1 ? go(flashsign_combine_kernel<FS_F16, FS_NORM_SIGNED_L1, DK>)
+         : go(flashsign_combine_kernel<FS_F16, FS_NORM_SPHERICAL, DK>);
+      break;
+    default:
+      return fail(FS_ERR_DTYPE, "out_dtype must be FS_F32, FS_BF16 or FS_F16");
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("combine launch: ") + cudaGetErrorString(e));
+  return FS_OK;
+}
+
 template <int IN, int D, int OUT, int NORM, bool KS>
 static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   using C = Cfg<IN, D>;
@@ -812,16 +931,26 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   kp.bad_key = p->bad_key;
   const double pmax = InTraits<IN>::PMAX / std::fabs((double)p->p_scale);
   kp.ovf_z = (float)std::fmin(NORM == FS_NORM_SIGNED_L1 ? pmax : pmax * pmax, 3.0e38);
+  const SplitPlan sp = split_plan(p);
   const int64_t n_qblk = (p->seqlen_q + NQT * BM - 1) / (NQT * BM);
-  const int64_t n_tiles = n_qblk * p->heads_q * p->batch;
+  const int64_t n_tiles = n_qblk * sp.splits * p->heads_q * p->batch;
   if (n_tiles > INT32_MAX) return fail(FS_ERR_UNSUPPORTED, "too many work tiles for one launch");
   kp.n_qblk = (int32_t)n_qblk;
   kp.n_tiles = (int32_t)n_tiles;
+  kp.n_batch = p->batch;
+  kp.kv_splits = sp.splits;
+  kp.split_tiles = sp.split_tiles;
+  kp.n_kv_tiles = sp.n_kv_tiles;
+  const bool partial = sp.splits > 1 || p->partial_only;
+  const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
+  kp.part_num = partial ? p->partial : nullptr;
+  kp.part_z = partial ? p->partial + (int64_t)sp.splits * rows * D : nullptr;
   const int grid = (int)std::min<int64_t>(n_tiles, num_sms());
   if (grid <= 0) return fail(FS_ERR_CUDA, "no SMs reported for the current device");
   kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, tm, kp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  if (sp.splits > 1 && !p->partial_only) return combine<D>(p, sp.splits, stream);
   return FS_OK;
 }
 
@@ -875,7 +1004,29 @@ int fs_prof_read(unsigned long long* out8) {
 
 const char* fs_last_error(void) { return fs::g_last_error.c_str(); }
 
-int fs_version(void) { return 200; }
+int fs_version(void) { return 300; }
+
+int32_t fs_kv_splits(const fs_fwd_params* p) { return p ? fs::split_plan(p).splits : 0; }
+
+int64_t fs_partial_floats(const fs_fwd_params* p) {
+  if (!p) return 0;
+  const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
+  return (int64_t)fs::split_plan(p).splits * rows * (fs::kernel_d(p) + 1);
+}
+
+fs_status fs_combine(const fs_fwd_params* p, int32_t n_parts, fs_stream_t stream_) {
+  using namespace fs;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (!p || !p->partial || n_parts < 1) return fail(FS_ERR_CONFIG, "fs_combine needs `partial` and n_parts >= 1");
+  if (p->normalizer != FS_NORM_SPHERICAL && p->normalizer != FS_NORM_SIGNED_L1)
+    return fail(FS_ERR_CONFIG, "normalizer must be FS_NORM_SPHERICAL or FS_NORM_SIGNED_L1");
+  if (!(p->eps >= 0.0f) || !std::isfinite(p->eps)) return fail(FS_ERR_CONFIG, "denom_epsilon must be finite and >= 0");
+  if (p->bad_key) {
+    cudaError_t e = cudaMemsetAsync(p->bad_key, 0xFF, sizeof(uint64_t), stream);
+    if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
+  }
+  return kernel_d(p) == 128 ? combine<128>(p, n_parts, stream) : combine<64>(p, n_parts, stream);
+}
 
 int fs_query_tile(int head_dim, fs_dtype dt, int* bm, int* bn) {
   if (!bm || !bn || head_dim < 1 || head_dim > 128) return 1;
@@ -924,6 +1075,10 @@ fs_status fs_fwd(const fs_fwd_params* p, fs_stream_t stream_) {
     if (p->batch > 1 && (p->key_scale_stride < p->seqlen_kv || (p->key_scale_stride * 4) % 16 != 0))
       return fail(FS_ERR_UNSUPPORTED, "key_scale_stride must be >= seqlen_kv and a multiple of 4 elements");
   }
+  if (p->kv_splits < 0) return fail(FS_ERR_CONFIG, "kv_splits must be >= 0");
+  if ((split_plan(p).splits > 1 || p->partial_only) && (p->partial == nullptr || !aligned16(p->partial)))
+    return fail(FS_ERR_CONFIG, "kv_splits > 1 / partial_only need a 16-byte aligned `partial` workspace of "
+                               "fs_partial_floats(p) floats");
   if (p->bad_key) {
     cudaError_t e = cudaMemsetAsync(p->bad_key, 0xFF, sizeof(uint64_t), stream);
     if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));

@@ -80,7 +80,8 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
               q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0,
               bad_key: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
               tile_hint: tuple[int, int] = (0, 0), normalizer: str = "spherical",
-              key_scale: torch.Tensor | None = None):
+              key_scale: torch.Tensor | None = None, kv_splits: int | None = None,
+              partial: torch.Tensor | None = None, partial_only: bool = False):
     """Launch FlashSign and return ``(o, bad_key)`` without synchronising.
 
     ``bad_key`` is a 1-element int64 CUDA tensor holding the packed first bad
@@ -88,6 +89,10 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
     ``key_scale`` (optional): float32 CUDA tensor ``[B, Nkv]`` (or ``[Nkv]`` when
     B == 1) of per-key multiplicities, finite and >= 0 -- not validated here
     (``fwd(check=True)`` does, like attention.py:386-387).
+    ``kv_splits``: K/V ranges per (b, h) (None: automatic -- split only when the
+    (b, h, 256-row) work tiles cannot fill the GPU); ranges merge by plain addition
+    of (numerator, z) (streaming.py:122-128), in a second small kernel.
+    With ``partial_only`` the call returns ``(partial, n_parts)`` instead (see ``fwd_partial``).
     """
     _check_inputs(q, k, v)
     if normalizer not in NORMALIZERS:
@@ -132,15 +137,101 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
             ks = _padded_rows(ks)
         prm.key_scale, prm.key_scale_stride = ks.data_ptr(), ks.stride(0)
         key_scale = ks  # keep alive until the launch is enqueued
+    prm.kv_splits = int(auto_splits(b, h, nq, nkv, q.device, d) if kv_splits is None else kv_splits)
+    if prm.kv_splits < 0:
+        raise ConfigError(f"kv_splits must be >= 0, got {kv_splits}")
+    lib = _lib.load()
+    prm.partial_only = int(bool(partial_only))
+    if partial_only or lib.fs_kv_splits(ctypes.byref(prm)) > 1:
+        need = lib.fs_partial_floats(ctypes.byref(prm))
+        if partial is None:
+            partial = torch.empty(need, dtype=torch.float32, device=q.device)
+        elif partial.dtype != torch.float32 or partial.numel() < need or not partial.is_contiguous():
+            raise ShapeMismatchError(f"flashsign: partial workspace needs {need} contiguous float32 elements")
+        prm.partial = partial.data_ptr()
 
     if stream is None:
         with torch.cuda.device(q.device):
             stream = torch.cuda.current_stream()
-    lib = _lib.load()
     st = lib.fs_fwd(ctypes.byref(prm), ctypes.c_void_p(stream.cuda_stream))
     if st != _lib.FS_OK:
         raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
+    if partial_only:
+        return partial, lib.fs_kv_splits(ctypes.byref(prm))
     return out, bad_key
+
+
+_SMS: dict = {}
+
+
+def auto_splits(b: int, h: int, nq: int, nkv: int, device, d: int = 128) -> int:
+    """K/V splits for launches whose (b, h, 256-row) work tiles cannot fill the GPU (small batch,
+    long sequence).  Picks S minimising a wave model, in units of one K/V-tile step of one work
+    tile (~2 us at d=128 on B200):  ceil(tiles*S / SMs) * (L/S + 2)  [2 = per-tile prologue and
+    epilogue]  +  the combine pass (S partial rows of d+1 fp32, read at ~5 TB/s).  1 when the
+    tiles already cover the SMs."""
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _SMS:
+        _SMS[idx] = torch.cuda.get_device_properties(idx).multi_processor_count
+    sms = _SMS[idx]
+    tiles = -(-nq // 256) * h * b
+    n_kv = -(-nkv // 128)
+    if tiles == 0 or tiles >= sms or n_kv < 8:
+        return 1
+    dk = 128 if d > 64 else 64
+    step_s = 4.0 * 256 * 128 * dk / 8.0e12          # one K/V tile of one work tile on one SM
+    rows = b * h * nq
+
+    def cost(s_):
+        split_tiles = -(-n_kv // s_)
+        s_eff = -(-n_kv // split_tiles)
+        waves = -(-(tiles * s_eff) // sms)
+        comb = 0.0 if s_eff == 1 else s_eff * rows * (dk + 1) * 4 / 5.0e12 / step_s
+        return waves * (split_tiles + 2) + comb
+
+    return min(range(1, min(16, n_kv // 4) + 1), key=cost)
+
+
+def fwd_partial(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, **kw):
+    """Partial FlashSign over this K/V (shard): returns ``(partial, n_parts)`` -- the fp32
+    numerators and z of every query row (``include/flashsign.h``: ``partial_only``), to be
+    summed across K/V shards (e.g. ``all_reduce``) and normalised by ``combine``."""
+    kw.setdefault("kv_splits", 1)
+    return fwd_async(q, k, v, partial_only=True, **kw)
+
+
+def combine(partial: torch.Tensor, n_parts: int, like_q: torch.Tensor, *, out: torch.Tensor | None = None,
+            out_dtype: torch.dtype | None = None, eps: float = 0.0, normalizer: str = "spherical",
+            bad_key: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None, check: bool = True):
+    """O = sum_s num_s / b(sum_s z_s + eps) from (summed) partials of ``fwd_partial``; ``like_q``
+    gives the query shape/dtype.  Raises DegenerateDenominatorError when ``check``."""
+    if normalizer not in NORMALIZERS:
+        raise ConfigError(f"flashsign: normalizer must be one of {sorted(NORMALIZERS)}, got {normalizer!r}")
+    b, nq, h, d = like_q.shape
+    if out_dtype is None:
+        out_dtype = out.dtype if out is not None else (like_q.dtype if like_q.dtype in (torch.bfloat16, torch.float16)
+                                                       else torch.bfloat16)
+    if out is None:
+        out = torch.empty((b, nq, h, d), dtype=out_dtype, device=like_q.device)
+    if bad_key is None:
+        bad_key = torch.empty(1, dtype=torch.int64, device=like_q.device)
+    prm = _lib.FsFwdParams()
+    prm.o = out.data_ptr()
+    prm.o_stride[0], prm.o_stride[1], prm.o_stride[2] = out.stride(0), out.stride(1), out.stride(2)
+    prm.batch, prm.heads_q, prm.seqlen_q, prm.head_dim = b, h, nq, d
+    prm.in_dtype, prm.out_dtype = _IN_CODES[like_q.dtype], _OUT_CODES[out.dtype]
+    prm.eps, prm.normalizer = float(eps), NORMALIZERS[normalizer]
+    prm.partial, prm.bad_key = partial.data_ptr(), bad_key.data_ptr()
+    if stream is None:
+        with torch.cuda.device(like_q.device):
+            stream = torch.cuda.current_stream()
+    st = _lib.load().fs_combine(ctypes.byref(prm), int(n_parts), ctypes.c_void_p(stream.cuda_stream))
+    if st != _lib.FS_OK:
+        raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
+    if check:
+        raise_if_bad(bad_key, h, nq)
+    return out
 
 
 def _padded_rows(ks: torch.Tensor) -> torch.Tensor:
@@ -180,14 +271,15 @@ def raise_if_bad(bad_key: torch.Tensor, heads_q: int, seqlen_q: int):
 def fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float = 1.0, eps: float = 0.0,
         out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None, p_scale: float = 1.0,
         q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0, check: bool = True,
-        normalizer: str = "spherical", key_scale: torch.Tensor | None = None) -> torch.Tensor:
+        normalizer: str = "spherical", key_scale: torch.Tensor | None = None,
+        kv_splits: int | None = None) -> torch.Tensor:
     """FlashSign forward ``O = c*sum_j s_ij v_j / sqrt(c^2 sum_j s_ij^2 + eps)`` on BSHD CUDA tensors
     (``normalizer="signed_l1"``: ``/ (|c| sum_j |s_ij| + eps)``)."""
     if check and key_scale is not None:
         check_key_scale(key_scale)
     o, bad = fwd_async(q, k, v, scale=scale, eps=eps, out=out, out_dtype=out_dtype, p_scale=p_scale,
                        q_descale=q_descale, k_descale=k_descale, v_descale=v_descale, normalizer=normalizer,
-                       key_scale=key_scale)
+                       key_scale=key_scale, kv_splits=kv_splits)
     if check:
         raise_if_bad(bad, q.shape[2], q.shape[1])
     return o

@@ -88,6 +88,39 @@ def fwd_shard(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor
     return flags
 
 
+def kv_shard_range(n_kv: int, world: int, rank: int, align: int = 128) -> tuple[int, int]:
+    """Contiguous key range [lo, hi) of ``rank`` for context parallelism, cut at multiples of
+    ``align`` (the kernel's K/V tile) so no rank streams a partial tile it does not own."""
+    tiles = -(-n_kv // align)
+    lo_t, hi_t = unit_range(tiles, world, rank)
+    return min(n_kv, lo_t * align), min(n_kv, hi_t * align)
+
+
+def context_parallel_fwd(q: torch.Tensor, k_shard: torch.Tensor, v_shard: torch.Tensor, group=None, *,
+                         eps: float = 0.0, normalizer: str = "spherical", out_dtype=None, check: bool = True,
+                         fwd_partial=None, combine=None, **kw) -> torch.Tensor:
+    """Sequence-parallel FlashSign: every rank holds all queries and one
+    contiguous shard of the K/V sequence (``kv_shard_range``).
+
+    Spherical (and signed-L1) partials over disjoint key ranges merge by plain addition --
+    the numerator sum_j s_ij v_j and z = sum_j a2(s_ij) are both linear in the key set
+    (streaming.py:122-128) -- so one ``all_reduce(SUM)`` of the fp32
+    (numerator, z) workspace, d+1 floats per query row, replaces softmax ring attention's
+    max/rescale exchange.  Each rank then normalises locally; every rank returns the full O.
+    ``fwd_partial`` / ``combine`` default to the CUDA kernels (injectable for CPU tests).
+    """
+    import torch.distributed as dist
+
+    if fwd_partial is None or combine is None:
+        from . import flashsign
+        fwd_partial = fwd_partial or flashsign.fwd_partial
+        combine = combine or flashsign.combine
+    partial, n_parts = fwd_partial(q, k_shard, v_shard, eps=eps, normalizer=normalizer, **kw)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
+    return combine(partial, n_parts, q, eps=eps, normalizer=normalizer, out_dtype=out_dtype, check=check)
+
+
 def gather_output(o_local: torch.Tensor, group=None) -> torch.Tensor:
     """all_gather equal-size shard outputs (along batch) into one tensor on every rank."""
     import torch.distributed as dist

@@ -30,7 +30,7 @@ HEADER = os.path.join(ROOT, "include", "flashsign.h")
 
 def header_functions():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*[a-z_ ]+\**\s*\*?\s*(fs_[a-z_]+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*[a-z0-9_ ]+\**\s*\*?\s*(fs_[a-z_]+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_header_symbol():

@@ -587,3 +587,65 @@ def test_compat_fused_multiplicity_against_reference_golden(golden, tag):
         assert np.abs(got.astype(np.float64) - want).max() <= 8e-3 * max(1.0, float(np.abs(want).max()))
     else:
         check_rel(got, want, torch.float16, c)
+
+
+# ------------------------------------------------------------------ split K/V and context parallelism
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16, torch.float8_e4m3fn])
+@pytest.mark.parametrize("splits", [2, 3, 7])
+def test_kv_splits_match_oracle(dt, splits):
+    d = 128 if dt == torch.float8_e4m3fn else 64
+    q = rand_bshd(1, 300, 2, d, dt, 70)
+    k = rand_bshd(1, 1000, 1, d, dt, 71)
+    v = rand_bshd(1, 1000, 1, d, dt, 72)
+    o1 = fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, kv_splits=1)
+    os_ = fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, kv_splits=splits)
+    ref = oracle_of(q, k, v, 1.0, 1e-6)
+    check_tol(os_.cpu().numpy(), ref, dt, f"splits={splits}")
+    # only the summation order of the split partials differs from the single pass
+    assert float((os_ - o1).abs().max()) <= 2e-5 * max(1.0, float(o1.abs().max()))
+
+
+def test_kv_splits_signed_l1_and_degenerate_rows():
+    q = rand_bshd(2, 200, 2, 128, torch.bfloat16, 73)
+    k = rand_bshd(2, 900, 2, 128, torch.bfloat16, 74)
+    v = rand_bshd(2, 900, 2, 128, torch.bfloat16, 75)
+    o = fs().fwd(q, k, v, out_dtype=torch.float32, normalizer="signed_l1", kv_splits=4)
+    check_rel(o.cpu().numpy(), exact_of(q, k, v, 1.0, 0.0, "signed_l1"), torch.bfloat16, "l1 split")
+    q[1, 33, 0] = 0  # batch 1 head 0 row 33 -> z = 0 after the merge
+    q[1, 150, 1] = 0
+    _, bad = fs().fwd_async(q, k, v, kv_splits=4)
+    assert fs().decode_bad_key(int(bad.item()), 2, 200) == (1, 0, 33, 0.0)
+
+
+def test_auto_splits_small_batch_long_sequence():
+    # B*H*ceil(N/256) = 16 work tiles < 148 SMs -> the launch is split automatically
+    q = rand_bshd(1, 1024, 4, 128, torch.bfloat16, 76)
+    k = rand_bshd(1, 16384, 4, 128, torch.bfloat16, 77)
+    v = rand_bshd(1, 16384, 4, 128, torch.bfloat16, 78)
+    assert fs().auto_splits(1, 4, 1024, 16384, q.device) > 1
+    o = fs().fwd(q, k, v, out_dtype=torch.float32)
+    check_tol(o.cpu().numpy(), oracle_of(q, k, v), torch.bfloat16, "auto split")
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_context_parallel_emulated_on_one_gpu(world):
+    # the all_reduce(SUM) of the per-shard partial workspaces, done here by adding them
+    from paper_2505_09326_b200 import partition
+    q = rand_bshd(2, 257, 4, 128, torch.bfloat16, 79)
+    k = rand_bshd(2, 2000, 2, 128, torch.bfloat16, 80)
+    v = rand_bshd(2, 2000, 2, 128, torch.bfloat16, 81)
+    total, n_parts = None, None
+    for r in range(world):
+        lo, hi = partition.kv_shard_range(k.shape[1], world, r)
+        part, n = fs().fwd_partial(q, k[:, lo:hi], v[:, lo:hi], eps=1e-6)
+        total = part.clone() if total is None else total + part
+        assert n_parts in (None, n)
+        n_parts = n
+    o = fs().combine(total, n_parts, q, eps=1e-6, out_dtype=torch.float32)
+    check_tol(o.cpu().numpy(), oracle_of(q, k, v, 1.0, 1e-6), torch.bfloat16, f"cp world={world}")
+    full = fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32)
+    assert float((o - full).abs().max()) <= 2e-5 * max(1.0, float(full.abs().max()))
+    # single process: context_parallel_fwd without a process group is the plain partial + combine
+    o2 = partition.context_parallel_fwd(q, k, v, eps=1e-6, out_dtype=torch.float32)
+    assert float((o2 - full).abs().max()) <= 2e-5 * max(1.0, float(full.abs().max()))

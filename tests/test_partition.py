@@ -99,3 +99,67 @@ def test_gloo_world2_shards_gather_to_full_result():
     mp.spawn(_worker, args=(2, _free_port(), q, k, v, result), nprocs=2, join=True)
     want = gram_batched(q.numpy(), k.numpy(), v.numpy())
     np.testing.assert_allclose(result.numpy(), want, rtol=0, atol=0)
+
+
+# ---------------------------------------------------------------- context parallelism
+
+@pytest.mark.parametrize("n_kv,world", [(1000, 2), (128, 2), (5000, 8), (129, 3), (0, 2)])
+def test_kv_shard_ranges_tile_aligned_and_exact(n_kv, world):
+    rs = [partition.kv_shard_range(n_kv, world, r) for r in range(world)]
+    assert rs[0][0] == 0 and rs[-1][1] == n_kv
+    for (a, b), (c, d) in zip(rs, rs[1:]):
+        assert b == c
+    for a, b in rs:
+        assert a <= b and (a == b or a % 128 == 0)
+
+
+def _cpu_partial(q, k, v, eps=0.0, normalizer="spherical", **kw):
+    """CPU stand-in for flashsign.fwd_partial with the C-ABI workspace layout
+    (include/flashsign.h: numerators [S=1][B][H][Nq][Dk] then z [S][B][H][Nq], Dk = 64 here)."""
+    b, nq, h, d = q.shape
+    hkv = k.shape[2]
+    dk = 64
+    num = torch.zeros((b, h, nq, dk), dtype=torch.float64)
+    z = torch.zeros((b, h, nq), dtype=torch.float64)
+    for bb in range(b):
+        for hh in range(h):
+            g = hh * hkv // h
+            s = q[bb, :, hh].double() @ k[bb, :, g].double().T
+            num[bb, hh, :, :d] = s @ v[bb, :, g].double()
+            z[bb, hh] = (s * s).sum(1) if normalizer == "spherical" else s.abs().sum(1)
+    return torch.cat([num.flatten(), z.flatten()]), 1
+
+
+def _cpu_combine(ws, n_parts, like_q, eps=0.0, normalizer="spherical", out_dtype=None, check=True):
+    b, nq, h, d = like_q.shape
+    rows = b * h * nq
+    num = ws[: n_parts * rows * 64].view(n_parts, b, h, nq, 64).sum(0)
+    z = ws[n_parts * rows * 64: n_parts * rows * 65].view(n_parts, b, h, nq).sum(0)
+    den = (z + eps).sqrt() if normalizer == "spherical" else z + eps
+    return (num[..., :d] / den[..., None]).permute(0, 2, 1, 3).contiguous()
+
+
+def _cp_worker(rank, world, port, q, k, v, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = partition.kv_shard_range(k.shape[1], world, rank)
+    o = partition.context_parallel_fwd(q, k[:, lo:hi], v[:, lo:hi], eps=1e-6, fwd_partial=_cpu_partial,
+                                       combine=_cpu_combine)
+    result[rank].copy_(o)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_context_parallel_matches_full():
+    # each rank streams half of the keys; one all_reduce(SUM) of (numerator, z) -> the full result
+    torch.manual_seed(1)
+    B, N, H, HKV, D = 2, 40, 4, 2, 16
+    q = torch.randn(B, N, H, D, dtype=torch.float64)
+    k = torch.randn(B, 300, HKV, D, dtype=torch.float64)
+    v = torch.randn(B, 300, HKV, D, dtype=torch.float64)
+    result = torch.zeros((2,) + tuple(q.shape), dtype=torch.float64).share_memory_()
+    mp.spawn(_cp_worker, args=(2, _free_port(), q, k, v, result), nprocs=2, join=True)
+    want = gram_batched(q.numpy(), k.numpy(), v.numpy(), 1.0, 1e-6)
+    for r in range(2):
+        np.testing.assert_allclose(result[r].numpy(), want, rtol=1e-10, atol=1e-12)
