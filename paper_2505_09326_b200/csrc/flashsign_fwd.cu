@@ -12,7 +12,7 @@
 //                               K_j / V_j into a STAGES-deep ring that runs across work tiles
 //   warp 1       MMA issuer     S_t = Q_t K_j^T  (tcgen05 SS, S in TMEM, fp32)
 //                               O_t += P_t V_j   (tcgen05 TS: P read from TMEM, V MN-major),
-//                               issued in two K-halves, each as soon as its half of P is ready
+//                               issued once all of P_t is in TMEM
 //   warp 2       TMEM allocator (512 columns: S_0, S_1, O_0, O_1 [, second O set when d=64])
 //   warps 4-7    norm WG 0      row r of tile 0: z += sum s^2 (packed FFMA2, registers),
 //                               P = cvt(s) -> TMEM over S, half a tile at a time
@@ -65,6 +65,9 @@ constexpr int BN = 128;  // keys per K/V tile
 constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_NWT
 #define FS_NWT 8  // norm warps per Q tile: 8 (one per lane quarter x column half) or 4
+#endif
+#ifndef FS_KV1
+#define FS_KV1 1  // K_j and V_j share one ring barrier when the ring has 8 slots (see Cfg::KV1)
 #endif
 #ifndef FS_STAGES16
 #define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=64 16-bit, d=128 e4m3)
@@ -135,6 +138,10 @@ struct Cfg {
   // d=128 e4m3): Q double-buffered (the next work tile's Q lands during this one), 8 ring slots.
   static constexpr int NQB = (SLOT_BYTES >= 32768) ? 1 : 2;
   static constexpr int STAGES = (SLOT_BYTES >= 32768) ? 4 : FS_STAGES16;
+  // K_j and V_j share one ring barrier when the ring is deep (8 slots): one wait per K/V tile on
+  // the MMA issuer.  With 4 slots the pair would halve the prefetch distance (measured -10 % at C3).
+  static constexpr bool KV1 = FS_KV1 && STAGES >= 8;
+  __device__ static uint32_t kv_bar(uint32_t slot) { return KV1 ? (slot & ~1u) : slot; }
   static constexpr int RING_OFF = NQT * NQB * Q_TILE_BYTES;
   static constexpr int BAR_OFF = RING_OFF + STAGES * SLOT_BYTES;
   static constexpr int ZBUF_OFF = BAR_OFF + 512;
@@ -153,7 +160,7 @@ struct Cfg {
   static constexpr uint32_t COL_O0 = NSB * BN;
   static_assert(NSB * BN + NOB * NQT * D <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
-  static_assert(PV_STEPS % 2 == 0, "PV is issued in two K-halves");
+  static_assert(PV_STEPS % 2 == 0, "P is produced in two column halves");
   static constexpr uint32_t IDESC_QK = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, BM, BN);
   static constexpr uint32_t IDESC_PV = ptx::idesc_make(TR::FMT, TR::FMT, 0, 1, BM, D);
 };
@@ -162,7 +169,7 @@ struct Bars {
   uint64_t q_full[NQT][2], q_empty[NQT][2];
   uint64_t kv_full[8], kv_empty[8];
   uint64_t s_full[2];       // per S buffer (= Q tile)
-  uint64_t p_full[2][2];    // per S buffer and half of the P tile
+  uint64_t p_full[2];       // per S buffer: all 8 norm warps of the tile have written P
   uint64_t o_full[NQT][2], o_empty[NQT][2];
   uint64_t z_full[NQT][2], z_empty[NQT][2];
   uint32_t tmem_base;
@@ -266,8 +273,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&bars->s_full[b], 1);
-      ptx::mbar_init(&bars->p_full[b][0], 4);
-      ptx::mbar_init(&bars->p_full[b][1], 4);
+      ptx::mbar_init(&bars->p_full[b], 8);  // 2 column halves x 4 lane quarters
     }
 #pragma unroll
     for (int t = 0; t < NQT; ++t) {
@@ -344,17 +350,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int i = 0; i < 2 * L; ++i, ++kv_i) {
           const uint32_t slot = kv_i % C::STAGES;
           const uint32_t round = kv_i / C::STAGES;
-          ptx::mbar_wait(&bars->kv_empty[slot], (round & 1u) ^ 1u);
           const bool with_m = KS && (i & 1);  // V slots also carry the tile's key multiplicities
-          ptx::mbar_arrive_expect_tx(&bars->kv_full[slot], C::SLOT_BYTES + (with_m ? C::MS_SLOT_BYTES : 0));
+          uint64_t* full = &bars->kv_full[C::kv_bar(slot)];
+          if (!C::KV1 || !(i & 1)) {
+            ptx::mbar_wait(&bars->kv_empty[C::kv_bar(slot)], (round & 1u) ^ 1u);
+            // with KV1 the K load announces both tiles' bytes (V follows right after)
+            ptx::mbar_arrive_expect_tx(full, (C::KV1 ? 2 : 1) * C::SLOT_BYTES + (KS ? C::MS_SLOT_BYTES : 0) *
+                                                                                   (C::KV1 ? 1 : (i & 1)));
+          }
           const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
           const int key0 = (tc.kb0 + (i >> 1)) * BN;
           if (with_m)
-            ptx::tma_load_2d(smem + C::MS_OFF + slot * C::MS_SLOT_BYTES, &tm_m, &bars->kv_full[slot], key0,
-                             tc.batch, pol_kv);
+            ptx::tma_load_2d(smem + C::MS_OFF + slot * C::MS_SLOT_BYTES, &tm_m, full, key0, tc.batch, pol_kv);
 #pragma unroll
           for (int db = 0; db < C::NDB; ++db)
-            ptx::tma_load_4d(smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128), tm, &bars->kv_full[slot],
+            ptx::tma_load_4d(smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128), tm, full,
                              db * C::BOXW, key0, head_kv, tc.batch, pol_kv);
           if (i == q_next_at && next < p.n_tiles) load_q(next, it + 1);
         }
@@ -376,7 +386,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
       {
       uint32_t kv_i = 0;                 // ring position of this work tile's K_0
-      uint32_t p_use[NQT] = {0u, 0u};    // completed phases of p_full[t][*]
+      uint32_t p_use[NQT] = {0u, 0u};    // completed phases of p_full[t]
       int it = 0;
       for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
         const int qb = it % C::NQB;
@@ -398,38 +408,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ptx::mma_f16_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
           }
         };
-        // O_t += P_t V_j, one K-half at a time as the norm WG finishes that half of P
+        // O_t += P_t V_j once all of P_t is in TMEM (one hand-off per tile: every extra
+        // barrier round trip on the issuing warp costs more than it overlaps, measured)
         auto pv = [&](int t, uint32_t slot, int j) {
           if (j == 0) ptx::mbar_wait(&bars->o_empty[t][ob], (o_use & 1u) ^ 1u);
           const uint64_t b0 = v_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
           const uint32_t a_tmem = tmem + C::COL_S0 + t * BN;
           const uint32_t d_tmem = tmem + C::COL_O0 + (ob * NQT + t) * D;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
 #if FS_PROF
-            const long long tw0 = clock64();
+          const long long tw0 = clock64();
 #endif
-            ptx::mbar_wait(&bars->p_full[t][h], p_use[t] & 1u);
+          ptx::mbar_wait(&bars->p_full[t], p_use[t] & 1u);
 #if FS_PROF
-            pr_pw += clock64() - tw0;
-            ++pr_pn;
+          pr_pw += clock64() - tw0;
+          ++pr_pn;
 #endif
-            ptx::tc_fence_after();
-            if (leader) {
+          ptx::tc_fence_after();
+          if (leader) {
 #pragma unroll
-              for (int k2 = 0; k2 < C::PV_STEPS / 2; ++k2) {
-                const int ks = h * (C::PV_STEPS / 2) + k2;
-                const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
-                const uint32_t at = a_tmem + h * (BN / 2) + k2 * (TR::KSTEP * C::EB / 4);
-                const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
-                if constexpr (TR::F8)
-                  ptx::mma_f8_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
-                else
-                  ptx::mma_f16_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
-              }
+            for (int ks = 0; ks < C::PV_STEPS; ++ks) {
+              const int h = ks / (C::PV_STEPS / 2), k2 = ks % (C::PV_STEPS / 2);
+              const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
+              // P of column half h is packed into the first columns of S_t's half h
+              const uint32_t at = a_tmem + h * (BN / 2) + k2 * (TR::KSTEP * C::EB / 4);
+              const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
+              if constexpr (TR::F8)
+                ptx::mma_f8_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
+              else
+                ptx::mma_f16_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
             }
-            __syncwarp();
           }
+          __syncwarp();
           ++p_use[t];
         };
 #pragma unroll
@@ -442,7 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #if FS_PROF
           const long long tk0 = clock64();
 #endif
-          ptx::mbar_wait(&bars->kv_full[k_slot], (k_idx / C::STAGES) & 1u);
+          ptx::mbar_wait(&bars->kv_full[C::kv_bar(k_slot)], (k_idx / C::STAGES) & 1u);
 #if FS_PROF
           pr_kw += clock64() - tk0;
           ++pr_kn;
@@ -456,17 +465,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (j > 0) {
             pv(1, prev_v_slot, j - 1);
-            if (leader) ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
+            if (leader) ptx::tc_commit(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
             __syncwarp();
           }
           if (leader) {
             qk(1, k_slot);
             ptx::tc_commit(&bars->s_full[1]);
-            ptx::tc_commit(&bars->kv_empty[k_slot]);
+            if (!C::KV1) ptx::tc_commit(&bars->kv_empty[k_slot]);  // KV1: freed with V after PV1
             if (j == L - 1) ptx::tc_commit(&bars->q_empty[1][qb]);
           }
           __syncwarp();
-          ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
+          if (!C::KV1) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
           pv(0, v_slot, j);
           if (j == L - 1) {
             if (leader) ptx::tc_commit(&bars->o_full[0][ob]);
@@ -476,7 +485,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         pv(1, prev_v_slot, L - 1);
         if (leader) {
-          ptx::tc_commit(&bars->kv_empty[prev_v_slot]);
+          ptx::tc_commit(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
           ptx::tc_commit(&bars->o_full[1][ob]);
         }
         __syncwarp();
@@ -521,7 +530,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // key multiplicities of this K/V tile ride in V_j's ring slot; that slot is released only
         // after PV_1(j), which needs this warp's P, so they stay valid while they are read here
         const uint32_t v_idx = 2u * s_use + 1u, v_slot = v_idx % C::STAGES;
-        if constexpr (KS) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
+        if constexpr (KS) ptx::mbar_wait(&bars->kv_full[C::kv_bar(v_slot)], (v_idx / C::STAGES) & 1u);
         ++s_use;
 #if FS_PROF
         const long long tn1 = clock64();
@@ -609,7 +618,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&bars->p_full[sb][hh]);
+        if (lane == 0) ptx::mbar_arrive(&bars->p_full[sb]);
 #if FS_PROF
         pr_nc += clock64() - tn1;
         ++pr_nn;
