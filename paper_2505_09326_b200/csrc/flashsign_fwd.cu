@@ -69,6 +69,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_KV1
 #define FS_KV1 1  // K_j and V_j share one ring barrier when the ring has 8 slots (see Cfg::KV1)
 #endif
+#ifndef FS_STAGES32
+#define FS_STAGES32 4  // K/V ring depth for 32 KB slots (d=128 16-bit); 5 fits without multiplicities but measured equal
+#endif
 #ifndef FS_STAGES16
 #define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=64 16-bit, d=128 e4m3)
 #endif
@@ -124,7 +127,7 @@ struct InTraits<FS_E4M3> {
   static constexpr float PMAX = 448.0f;
 };
 
-template <int IN, int D>
+template <int IN, int D, bool KS = false>
 struct Cfg {
   using TR = InTraits<IN>;
   static constexpr int EB = TR::EB;
@@ -137,7 +140,9 @@ struct Cfg {
   // 32 KB slots (d=128, 16-bit): one Q buffer per tile, 4 ring slots.  16 KB slots (d=64 16-bit,
   // d=128 e4m3): Q double-buffered (the next work tile's Q lands during this one), 8 ring slots.
   static constexpr int NQB = (SLOT_BYTES >= 32768) ? 1 : 2;
-  static constexpr int STAGES = (SLOT_BYTES >= 32768) ? 4 : FS_STAGES16;
+  // (32 KB slots: a fifth slot fits when no per-key multiplicity ring is needed and the dynamic
+  //  shared-memory base is 1024-aligned -- checked on the device, see SLACK)
+  static constexpr int STAGES = (SLOT_BYTES >= 32768) ? (KS ? 4 : FS_STAGES32) : FS_STAGES16;
   // K_j and V_j share one ring barrier when the ring is deep (8 slots): one wait per K/V tile on
   // the MMA issuer.  With 4 slots the pair would halve the prefetch distance (measured -10 % at C3).
   static constexpr bool KV1 = FS_KV1 && STAGES >= 8;
@@ -153,7 +158,10 @@ struct Cfg {
   // per-key multiplicities m_j of each V slot's keys (fused K' = m K, grn.py:150)
   static constexpr int MS_OFF = ZBUF_OFF + NQT * NOB * 2 * BM * 4;
   static constexpr int MS_SLOT_BYTES = BN * 4;
-  static constexpr int SMEM_BYTES = MS_OFF + STAGES * MS_SLOT_BYTES + 1024;  // + alignment slack
+  static constexpr int LAYOUT_BYTES = MS_OFF + (KS ? STAGES * MS_SLOT_BYTES : 0);
+  // 1024-byte alignment slack for the SW128 buffers when it fits; else the base must be aligned
+  static constexpr int SLACK = (LAYOUT_BYTES + 1024 <= 232448) ? 1024 : 0;
+  static constexpr int SMEM_BYTES = LAYOUT_BYTES + SLACK;
   static constexpr int QK_STEPS = ROW_BYTES / 32;                          // 32 B of K-dim per MMA
   static constexpr int PV_STEPS = BN / TR::KSTEP;
   static constexpr uint32_t COL_S0 = 0;
@@ -256,10 +264,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     flashsign_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_m,
                          const KParams p) {
-  using C = Cfg<IN, D>;
+  using C = Cfg<IN, D, KS>;
   using TR = InTraits<IN>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_s = ptx::smem_u32(smem_raw);
+  if (C::SLACK == 0 && (raw_s & 1023u) != 0) __trap();  // layout needs an aligned base (see Cfg::SLACK)
   uint8_t* smem = smem_raw + ((1024u - (raw_s & 1023u)) & 1023u);
   const uint32_t smem_s = ptx::smem_u32(smem);
   Bars* bars = reinterpret_cast<Bars*>(smem + C::BAR_OFF);
@@ -377,6 +386,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // lane issues.  Descriptors are built once; per-step offsets are constants.
     if (n_kv_tiles > 0) {
       const bool leader = ptx::elect_one();
+      // every lane runs the issue code; the elected lane's predicate makes it the only issuer
+      const uint32_t lp = leader ? 1u : 0u;
       const uint64_t q_desc = ptx::sdesc_sw128(smem_s, 16, 1024);
       const uint64_t k_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, 16, 1024);
       const uint64_t v_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, BN * 128, 1024);
@@ -403,9 +414,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t off_a = ((ks * 32 / 128) * (BM * 128) + (ks * 32) % 128) >> 4;
             const uint32_t off_b = ((ks * 32 / 128) * (BN * 128) + (ks * 32) % 128) >> 4;
             if constexpr (TR::F8)
-              ptx::mma_f8_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
+              ptx::mma_f8_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
             else
-              ptx::mma_f16_ss(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0);
+              ptx::mma_f16_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
           }
         };
         // O_t += P_t V_j once all of P_t is in TMEM (one hand-off per tile: every extra
@@ -424,21 +435,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ++pr_pn;
 #endif
           ptx::tc_fence_after();
-          if (leader) {
 #pragma unroll
-            for (int ks = 0; ks < C::PV_STEPS; ++ks) {
-              const int h = ks / (C::PV_STEPS / 2), k2 = ks % (C::PV_STEPS / 2);
-              const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
-              // P of column half h is packed into the first columns of S_t's half h
-              const uint32_t at = a_tmem + h * (BN / 2) + k2 * (TR::KSTEP * C::EB / 4);
-              const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
-              if constexpr (TR::F8)
-                ptx::mma_f8_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
-              else
-                ptx::mma_f16_ts(d_tmem, at, b0 + off_b, C::IDESC_PV, acc);
-            }
+          for (int ks = 0; ks < C::PV_STEPS; ++ks) {
+            const int h = ks / (C::PV_STEPS / 2), k2 = ks % (C::PV_STEPS / 2);
+            const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
+            // P of column half h is packed into the first columns of S_t's half h
+            const uint32_t at = a_tmem + h * (BN / 2) + k2 * (TR::KSTEP * C::EB / 4);
+            const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
+            if constexpr (TR::F8)
+              ptx::mma_f8_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
+            else
+              ptx::mma_f16_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
           }
-          __syncwarp();
           ++p_use[t];
         };
 #pragma unroll
@@ -457,38 +465,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ++pr_kn;
 #endif
           ptx::tc_fence_after();
-          if (leader) {
-            qk(0, k_slot);
-            ptx::tc_commit(&bars->s_full[0]);
-            if (j == L - 1) ptx::tc_commit(&bars->q_empty[0][qb]);
-          }
-          __syncwarp();
+          qk(0, k_slot);
+          ptx::tc_commit_p(&bars->s_full[0], lp);
+          if (j == L - 1) ptx::tc_commit_p(&bars->q_empty[0][qb], lp);
           if (j > 0) {
             pv(1, prev_v_slot, j - 1);
-            if (leader) ptx::tc_commit(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
-            __syncwarp();
+            ptx::tc_commit_p(&bars->kv_empty[C::kv_bar(prev_v_slot)], lp);
           }
-          if (leader) {
-            qk(1, k_slot);
-            ptx::tc_commit(&bars->s_full[1]);
-            if (!C::KV1) ptx::tc_commit(&bars->kv_empty[k_slot]);  // KV1: freed with V after PV1
-            if (j == L - 1) ptx::tc_commit(&bars->q_empty[1][qb]);
-          }
-          __syncwarp();
+          qk(1, k_slot);
+          ptx::tc_commit_p(&bars->s_full[1], lp);
+          if (!C::KV1) ptx::tc_commit_p(&bars->kv_empty[k_slot], lp);  // KV1: freed with V after PV1
+          if (j == L - 1) ptx::tc_commit_p(&bars->q_empty[1][qb], lp);
           if (!C::KV1) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
           pv(0, v_slot, j);
-          if (j == L - 1) {
-            if (leader) ptx::tc_commit(&bars->o_full[0][ob]);
-            __syncwarp();
-          }
+          if (j == L - 1) ptx::tc_commit_p(&bars->o_full[0][ob], lp);
           prev_v_slot = v_slot;
         }
         pv(1, prev_v_slot, L - 1);
-        if (leader) {
-          ptx::tc_commit(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
-          ptx::tc_commit(&bars->o_full[1][ob]);
-        }
-        __syncwarp();
+        ptx::tc_commit_p(&bars->kv_empty[C::kv_bar(prev_v_slot)], lp);
+        ptx::tc_commit_p(&bars->o_full[1][ob], lp);
         kv_i += 2 * L;
       }
       }
@@ -898,7 +893,7 @@ static fs_status combine(const fs_fwd_params* p, int n_parts, cudaStream_t strea
 
 template <int IN, int D, int OUT, int NORM, bool KS>
 static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
-  using C = Cfg<IN, D>;
+  using C = Cfg<IN, D, KS>;
   auto kern = flashsign_fwd_kernel<IN, D, OUT, NORM, KS>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;

@@ -229,6 +229,55 @@ __device__ __forceinline__ void mma_f8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       : "memory");
 }
 
+
+// ---- predicated forms: every lane of the issuing warp executes the instruction, only the lane
+// with pred != 0 issues it -- no divergent branch around the issue (no BSSY/BSYNC reconvergence)
+__device__ __forceinline__ void tc_commit_p(uint64_t* bar, uint32_t pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ne.b32 q, %1, 0;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(pred)
+      : "memory");
+}
+
+#define FS_MMA_P(NAME, KIND, AOP, ATYPE)                                                                     \
+  __device__ __forceinline__ void NAME(uint32_t d_tmem, ATYPE a, uint64_t b_desc, uint32_t idesc,           \
+                                       uint32_t accumulate, uint32_t pred) {                                \
+    asm volatile(                                                                                           \
+        "{\n\t.reg .pred p, q;\n\t"                                                                     \
+        "setp.ne.b32 p, %4, 0;\n\t"                                                                       \
+        "setp.ne.b32 q, %5, 0;\n\t"                                                                       \
+        "@q tcgen05.mma.cta_group::1.kind::" KIND " [%0], " AOP ", %2, %3, p;\n\t}" ::"r"(d_tmem),          \
+        "l"(a), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(pred)                                       \
+        : "memory");                                                                                        \
+  }
+FS_MMA_P(mma_f16_ss_p, "f16", "%1", uint64_t)
+FS_MMA_P(mma_f8_ss_p, "f8f6f4", "%1", uint64_t)
+#undef FS_MMA_P
+
+__device__ __forceinline__ void mma_f16_ts_p(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate, uint32_t pred) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(pred)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_f8_ts_p(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate, uint32_t pred) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(pred)
+      : "memory");
+}
+
 #define FS_R8(i) "=r"(r[i + 0]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3]), "=r"(r[i + 4]), "=r"(r[i + 5]), \
                  "=r"(r[i + 6]), "=r"(r[i + 7])
 #define FS_W8(i) "r"(r[i + 0]), "r"(r[i + 1]), "r"(r[i + 2]), "r"(r[i + 3]), "r"(r[i + 4]), "r"(r[i + 5]), \
