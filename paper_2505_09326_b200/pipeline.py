@@ -1,9 +1,12 @@
 """FlashSign on host-resident inputs: chunked H2D -> kernel -> D2H with overlap.
 
 ``fwd_host(q, k, v, out)`` takes pinned CPU tensors in BSHD layout (the
-compute dtype, e.g. bf16) and streams them through the GPU one batch chunk at
-a time on three CUDA streams -- copy-in, compute, copy-out -- so PCIe
-transfers of chunk i+1 and i-1 overlap the kernel on chunk i.  Device staging
+compute dtype, e.g. bf16) and streams them through the GPU on three CUDA
+streams -- copy-in, compute, copy-out -- so PCIe transfers overlap the kernel.
+The unit of the pipeline is a query slice of one batch chunk: K/V of the batch
+chunk go over first, then its queries in ``q_split`` row slices, each launched
+as soon as it lands, so the pipeline fills after ~1/(chunks * q_split) of the
+data instead of a whole batch row and drains after one slice.  Device staging
 buffers are double-buffered and reused across calls (``HostPipeline``).
 
 This is the end-to-end path a caller with host data uses (what the reference's
@@ -20,27 +23,37 @@ from . import flashsign
 class HostPipeline:
     """Reusable device staging for ``fwd_host`` (two slots per tensor)."""
 
-    def __init__(self, device: torch.device | int | None = None, chunk: int = 1):
+    def __init__(self, device: torch.device | int | None = None, chunk: int = 1, q_split: int | None = None):
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
                                    (device if isinstance(device, int) else device.index))
         self.chunk = chunk
+        self.q_split = q_split
         self._shape_key = None
         self.s_in = torch.cuda.Stream(self.device)
         self.s_cmp = torch.cuda.Stream(self.device)
         self.s_out = torch.cuda.Stream(self.device)
 
+    def _slices(self, nq: int) -> list[tuple[int, int]]:
+        # query slices of >= 1024 rows (4 work tiles per head), at most 4 per batch chunk
+        qs = self.q_split if self.q_split is not None else max(1, min(4, nq // 1024))
+        step = -(-nq // qs)
+        step = -(-step // 256) * 256  # whole 256-row work tiles
+        return [(n0, min(nq, n0 + step)) for n0 in range(0, nq, step)] or [(0, 0)]
+
     def _alloc(self, q, k, out, key_scale=None):
-        key = (tuple(q.shape[1:]), tuple(k.shape[1:]), q.dtype, out.dtype, self.chunk,
+        sl = self._slices(q.shape[1])
+        qmax = max(b - a for a, b in sl)
+        key = (tuple(q.shape[1:]), tuple(k.shape[1:]), q.dtype, out.dtype, self.chunk, qmax,
                None if key_scale is None else tuple(key_scale.shape[1:]))
         if key == self._shape_key:
             return
         c = self.chunk
         dev = self.device
-        self.dq = [torch.empty((c,) + tuple(q.shape[1:]), dtype=q.dtype, device=dev) for _ in range(2)]
+        qs = (c, qmax) + tuple(q.shape[2:])
+        self.dq = [torch.empty(qs, dtype=q.dtype, device=dev) for _ in range(2)]
         self.dk = [torch.empty((c,) + tuple(k.shape[1:]), dtype=k.dtype, device=dev) for _ in range(2)]
         self.dv = [torch.empty((c,) + tuple(k.shape[1:]), dtype=k.dtype, device=dev) for _ in range(2)]
-        self.do = [torch.empty((c,) + tuple(out.shape[1:]), dtype=out.dtype, device=dev) for _ in range(2)]
-        self.bad = [torch.empty(1, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.do = [torch.empty(qs, dtype=out.dtype, device=dev) for _ in range(2)]
         self.dm = None if key_scale is None else [
             torch.empty((c,) + tuple(key_scale.shape[1:]), dtype=torch.float32, device=dev) for _ in range(2)]
         self._shape_key = key
@@ -55,48 +68,72 @@ class HostPipeline:
             flashsign.check_key_scale(key_scale)
         self._alloc(q, k, out, key_scale)
         c = self.chunk
-        nb = q.shape[0]
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_cmp = [torch.cuda.Event() for _ in range(2)]
-        ev_out = [None, None]
+        nb, nq, h = q.shape[0], q.shape[1], q.shape[2]
+        slices = self._slices(nq)
+        ev_q_free = [None, None]     # compute done with Q slot / O slot producer side
+        ev_o_free = [None, None]     # D2H of O slot done
+        ev_kv_free = [None, None]    # last compute of a batch chunk done with its K/V slot
         bad_hits = []
+        g = 0                        # global slice counter -> Q / O slot
         with torch.cuda.device(self.device):
-            for i, b0 in enumerate(range(0, nb, c)):
-                s = i & 1
+            for ci, b0 in enumerate(range(0, nb, c)):
+                kvs = ci & 1
                 b1 = min(b0 + c, nb)
                 n = b1 - b0
+                ev_kv = torch.cuda.Event()
                 with torch.cuda.stream(self.s_in):
-                    if ev_out[s] is not None:  # slot s's previous output has left the device
-                        self.s_in.wait_event(ev_out[s])
-                    self.dq[s][:n].copy_(q[b0:b1], non_blocking=True)
-                    self.dk[s][:n].copy_(k[b0:b1], non_blocking=True)
-                    self.dv[s][:n].copy_(v[b0:b1], non_blocking=True)
+                    if ev_kv_free[kvs] is not None:
+                        self.s_in.wait_event(ev_kv_free[kvs])
+                    self.dk[kvs][:n].copy_(k[b0:b1], non_blocking=True)
+                    self.dv[kvs][:n].copy_(v[b0:b1], non_blocking=True)
                     if key_scale is not None:
-                        self.dm[s][:n].copy_(key_scale[b0:b1], non_blocking=True)
-                    ev_in[s].record(self.s_in)
-                with torch.cuda.stream(self.s_cmp):
-                    self.s_cmp.wait_event(ev_in[s])
-                    _, bad = flashsign.fwd_async(self.dq[s][:n], self.dk[s][:n], self.dv[s][:n], scale=scale,
-                                                 eps=eps, out=self.do[s][:n], bad_key=self.bad[s],
-                                                 stream=self.s_cmp,
-                                                 key_scale=None if key_scale is None else self.dm[s][:n], **kw)
-                    if check:
-                        bad_hits.append((b0, bad.clone()))
-                    ev_cmp[s].record(self.s_cmp)
-                with torch.cuda.stream(self.s_out):
-                    self.s_out.wait_event(ev_cmp[s])
-                    out[b0:b1].copy_(self.do[s][:n], non_blocking=True)
-                    e = torch.cuda.Event()
-                    e.record(self.s_out)
-                    ev_out[s] = e
+                        self.dm[kvs][:n].copy_(key_scale[b0:b1], non_blocking=True)
+                    ev_kv.record(self.s_in)
+                for (n0, n1) in slices:
+                    s = g & 1
+                    g += 1
+                    nn = n1 - n0
+                    ev_in = torch.cuda.Event()
+                    with torch.cuda.stream(self.s_in):
+                        if ev_q_free[s] is not None:
+                            self.s_in.wait_event(ev_q_free[s])
+                        self.dq[s][:n, :nn].copy_(q[b0:b1, n0:n1], non_blocking=True)
+                        ev_in.record(self.s_in)
+                    ev_cmp = torch.cuda.Event()
+                    with torch.cuda.stream(self.s_cmp):
+                        self.s_cmp.wait_event(ev_kv)
+                        self.s_cmp.wait_event(ev_in)
+                        if ev_o_free[s] is not None:  # slot s's previous output has left the device
+                            self.s_cmp.wait_event(ev_o_free[s])
+                        _, bad = flashsign.fwd_async(self.dq[s][:n, :nn], self.dk[kvs][:n], self.dv[kvs][:n],
+                                                     scale=scale, eps=eps, out=self.do[s][:n, :nn],
+                                                     stream=self.s_cmp,
+                                                     key_scale=None if key_scale is None else self.dm[kvs][:n],
+                                                     **kw)
+                        if check:
+                            bad_hits.append((b0, n0, nn, bad))
+                        ev_cmp.record(self.s_cmp)
+                    ev_q_free[s] = ev_cmp
+                    with torch.cuda.stream(self.s_out):
+                        self.s_out.wait_event(ev_cmp)
+                        out[b0:b1, n0:n1].copy_(self.do[s][:n, :nn], non_blocking=True)
+                        e = torch.cuda.Event()
+                        e.record(self.s_out)
+                        ev_o_free[s] = e
+                ev_kv_free[kvs] = ev_cmp
             self.s_out.synchronize()
             self.s_cmp.synchronize()
-        for b0, bad in bad_hits:
-            info = flashsign.decode_bad_key(int(bad.item()), q.shape[2], q.shape[1])
+        first = None  # the reference's loop order: batch, head, row
+        for b0, n0, nn, bad in bad_hits:
+            info = flashsign.decode_bad_key(int(bad.item()), h, nn)
             if info is not None:
-                _, _, row, z = info
-                from .normalizers import DegenerateDenominatorError
-                raise DegenerateDenominatorError(float(z), f"row {row}")
+                b, hh, row, z = info
+                key = ((b0 + b) * h + hh, n0 + row)
+                if first is None or key < first[0]:
+                    first = (key, z)
+        if first is not None:
+            from .normalizers import DegenerateDenominatorError
+            raise DegenerateDenominatorError(float(first[1]), f"row {first[0][1]}")
         return out
 
 

@@ -440,9 +440,17 @@ def test_host_pipeline_equals_device_path():
     ref = fs().fwd(q, k, v)
     qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
     oh = torch.empty(q.shape, dtype=torch.bfloat16, pin_memory=True)
-    for chunk in (1, 2):
-        HostPipeline(0, chunk=chunk).run(qh, kh, vh, oh)
-        assert torch.equal(oh, ref.cpu())
+    for chunk, qs in ((1, None), (2, None), (1, 3), (2, 2)):
+        oh.zero_()
+        HostPipeline(0, chunk=chunk, q_split=qs).run(qh, kh, vh, oh)
+        assert torch.equal(oh, ref.cpu()), (chunk, qs)
+    # the first degenerate row in (batch, head, row) order, across batch chunks and query slices
+    from paper_2505_09326_b200.normalizers import DegenerateDenominatorError
+    qh[3, 650, 1] = 0
+    qh[3, 20, 3] = 0
+    qh[4, 5, 0] = 0
+    with pytest.raises(DegenerateDenominatorError, match="row 650"):
+        HostPipeline(0, chunk=1, q_split=3).run(qh, kh, vh, oh)
 
 
 # ------------------------------------------------------------------ SIGNED_L1 and fused key multiplicities
