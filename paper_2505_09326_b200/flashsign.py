@@ -288,3 +288,29 @@ def fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float = 1.0
 def flops(batch: int, heads: int, n_q: int, n_kv: int, d: int) -> int:
     """Algorithmic FLOPs of one forward, 4*B*H*Nq*Nkv*d (costmodel.py:129)."""
     return 4 * batch * heads * n_q * n_kv * d
+
+
+class CapturedFwd:
+    """A FlashSign forward captured once into a CUDA graph and replayed.
+
+    For repeated calls on fixed shapes (e.g. every layer of a GRN forward), the host work of
+    ``fwd_async`` -- validation, three TMA descriptor encodes, the bad-row reset and the launch --
+    is paid once at capture; ``replay()`` is one graph launch.  Inputs are read from the
+    tensors given at construction (copy new data into them); ``out`` / ``bad_key`` are the
+    graph's outputs.
+    """
+
+    def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, **kw):
+        self.q, self.k, self.v = q, k, v
+        side = torch.cuda.Stream(q.device)
+        side.wait_stream(torch.cuda.current_stream(q.device))
+        with torch.cuda.stream(side):  # warm-up launch outside the capture (loads the module)
+            fwd_async(q, k, v, **kw)
+        torch.cuda.current_stream(q.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out, self.bad_key = fwd_async(q, k, v, **kw)
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.out

@@ -657,3 +657,19 @@ def test_context_parallel_emulated_on_one_gpu(world):
     # single process: context_parallel_fwd without a process group is the plain partial + combine
     o2 = partition.context_parallel_fwd(q, k, v, eps=1e-6, out_dtype=torch.float32)
     assert float((o2 - full).abs().max()) <= 2e-5 * max(1.0, float(full.abs().max()))
+
+
+def test_cuda_graph_capture_and_replay():
+    # fs_fwd is capturable (memset node + kernel node); replays see new input data
+    q = rand_bshd(2, 300, 4, 128, torch.bfloat16, 90)
+    k = rand_bshd(2, 517, 2, 128, torch.bfloat16, 91)
+    v = rand_bshd(2, 517, 2, 128, torch.bfloat16, 92)
+    cap = fs().CapturedFwd(q, k, v, out_dtype=torch.float32)
+    o1 = cap.replay().clone()
+    assert torch.equal(o1, fs().fwd(q, k, v, out_dtype=torch.float32))
+    q.copy_(rand_bshd(2, 300, 4, 128, torch.bfloat16, 93))
+    o2 = cap.replay().clone()
+    assert torch.equal(o2, fs().fwd(q, k, v, out_dtype=torch.float32))
+    assert not torch.equal(o1, o2)
+    torch.cuda.synchronize()
+    assert fs().decode_bad_key(int(cap.bad_key.item()), 4, 300) is None
