@@ -673,3 +673,32 @@ def test_cuda_graph_capture_and_replay():
     assert not torch.equal(o1, o2)
     torch.cuda.synchronize()
     assert fs().decode_bad_key(int(cap.bad_key.item()), 4, 300) is None
+
+
+# ------------------------------------------------------------------ per-tensor scales (FP8 quantisation recipe)
+
+def test_fp8_descales_and_p_scale():
+    # real q, k, v stored as e4m3 codes x / s with per-tensor descales s; P = p_scale * s_ij before
+    # the PV MMA (kept inside the e4m3 range), output divided by p_scale again (include/flashsign.h)
+    g = torch.Generator(device="cuda").manual_seed(94)
+    q, k, v = (torch.randn((2, 300, 2, 128), generator=g, device="cuda") for _ in range(3))
+    sq, sk, sv, ps = 0.25, 0.25, 0.5, 0.2
+    q8, k8, v8 = ((t / s).to(torch.float8_e4m3fn) for t, s in ((q, sq), (k, sk), (v, sv)))
+    o = fs().fwd(q8, k8, v8, q_descale=sq, k_descale=sk, v_descale=sv, p_scale=ps, out_dtype=torch.float32)
+    deq = [t.float() * s for t, s in ((q8, sq), (k8, sk), (v8, sv))]
+    check_tol(o.cpu().numpy(), oracle_of(*deq), torch.float8_e4m3fn, "fp8 descales")
+    # same P range without p_scale saturates e4m3 (|q8 . k8| > 448): reported as z = +inf
+    _, bad = fs().fwd_async(q8, k8, v8, q_descale=sq, k_descale=sk, v_descale=sv, p_scale=1.0)
+    info = fs().decode_bad_key(int(bad.item()), 2, 300)
+    assert info is not None and np.isinf(info[3])
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+def test_16bit_descales_and_p_scale(dt):
+    q = rand_bshd(1, 256, 2, 64, dt, 95)
+    k = rand_bshd(1, 300, 2, 64, dt, 96)
+    v = rand_bshd(1, 300, 2, 64, dt, 97)
+    o = fs().fwd(q, k, v, scale=0.5, q_descale=2.0, k_descale=0.5, v_descale=4.0, p_scale=0.25,
+                 out_dtype=torch.float32)
+    ref = oracle_of(q.float() * 2.0, k.float() * 0.5, v.float() * 4.0, 0.5)
+    check_tol(o.cpu().numpy() / 4.0, ref / 4.0, dt, f"{dt} descales")
