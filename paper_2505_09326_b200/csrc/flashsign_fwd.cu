@@ -5,20 +5,25 @@
 // (attention.py:252-279, 318-361).  Contract (normalizers.py:94-100):
 //     O_i = c * sum_j s_ij v_j / sqrt(c^2 * sum_j s_ij^2 + eps),   s_ij = q_i . k_j
 //
-// Persistent kernel: one CTA per SM walks work tiles (batch, head, 256 query rows =
-// NQT=2 query tiles of BM=128) with a static stride.  Roles (512 threads):
+// Persistent kernel: one CTA per SM walks work tiles (batch, head, K/V range, 256 query
+// rows = NQT=2 query tiles of BM=128) with a static stride.  Roles (768 threads):
 //
 //   warp 0       TMA producer   Q tiles of the next work tile as soon as their buffer frees,
 //                               K_j / V_j into a STAGES-deep ring that runs across work tiles
 //   warp 1       MMA issuer     S_t = Q_t K_j^T  (tcgen05 SS, S in TMEM, fp32)
 //                               O_t += P_t V_j   (tcgen05 TS: P read from TMEM, V MN-major),
-//                               issued once all of P_t is in TMEM
+//                               issued once all of P_t is in TMEM; every lane runs the
+//                               issue code, the elected lane's predicate makes it the issuer
 //   warp 2       TMEM allocator (512 columns: S_0, S_1, O_0, O_1 [, second O set when d=64])
-//   warps 4-7    norm WG 0      row r of tile 0: z += sum s^2 (packed FFMA2, registers),
-//                               P = cvt(s) -> TMEM over S, half a tile at a time
-//   warps 8-11   norm WG 1      same for tile 1, ping-ponging with WG 0
-//   warps 12-15  epilogue WG    O_t -> registers (frees TMEM for the next work tile),
-//                               O = acc * c / sqrt(c^2 z + eps) -> global
+//   warps 4-11   norm, tile 0   warp (column half h, lane quarter) owns 32 rows x 64 scores of
+//                               S_0: z += a2(s) (packed FFMA2/FADD2, registers), P = cvt(s) ->
+//                               TMEM in place (first columns of its own half of S)
+//   warps 12-19  norm, tile 1   same for S_1, ping-ponging with tile 0
+//   warps 20-23  epilogue WG    O_t -> registers (frees TMEM for the next work tile),
+//                               O = acc * c / b(z + eps) -> global, or fp32 partials (split K/V)
+//
+// Normalisers (compile-time NORM): spherical (a2 = s^2, b = sqrt) and signed L1 (a2 = |s|,
+// b = id), normalizers.py:94-117.  KS: per-key multiplicities m_j scale the scores in fp32.
 //
 // Spherical normalisation has no exp and no running max, so O never needs
 // rescaling: it stays in TMEM for the whole K/V stream and is scaled exactly
@@ -26,7 +31,7 @@
 // Zero padding is exact (a1(0)=a2(0)=0), so ragged N uses TMA out-of-bounds
 // zero fill, no masking.
 //
-// MMA issue order per K/V tile j (keeps each norm WG a full two-MMA window):
+// MMA issue order per K/V tile j (keeps each tile's norm warps a full two-MMA window):
 //     QK0(j)  PV1(j-1)  QK1(j)  PV0(j)
 // tcgen05 MMAs from one thread execute in issue order, so QK_t(j+1) may be
 // issued right after PV_t(j) although both touch S_t's columns (P aliases S).
