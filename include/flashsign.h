@@ -82,7 +82,9 @@ typedef struct {
        (linear_row << 32) | float_bits(z),  linear_row = (b*heads_q + h)*seqlen_q + n
      over rows whose denominator b(z + eps) is 0 or non-finite, i.e. the
      first bad row in the reference's loop order (batch, head, row) and its z
-     = sum_j a2(s_ij).  An FP16/FP8 P overflow is reported as z = +inf. */
+     = sum_j a2(s_ij).  A P that does not fit the MMA dtype is reported as z = +inf
+     (and the row's O is zeroed): FP16 P overflowing to inf (|p_scale s| >= 65520), FP8 P
+     saturating the e4m3 range (|p_scale s| >= 432, i.e. rounded to +-448). */
   uint64_t *bad_key;
   int32_t tile_m_hint, tile_n_hint; /* TileConfig (g_y, s_x); advisory only    */
   int32_t normalizer;               /* fs_normalizer; 0 = SPHERICAL            */

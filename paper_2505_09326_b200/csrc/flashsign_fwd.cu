@@ -74,6 +74,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_KV1
 #define FS_KV1 1  // K_j and V_j share one ring barrier when the ring has 8 slots (see Cfg::KV1)
 #endif
+#ifndef FS_NO_OVF
+#define FS_NO_OVF 0  // experiment knob: skip the fp16 P-overflow check
+#endif
 #ifndef FS_STAGES32
 #define FS_STAGES32 4  // K/V ring depth for 32 KB slots (d=128 16-bit); 5 fits without multiplicities but measured equal
 #endif
@@ -114,22 +117,27 @@ template <>
 struct InTraits<FS_BF16> {
   static constexpr int EB = 2, KSTEP = 16;
   static constexpr uint32_t FMT = 1;
-  static constexpr bool F8 = false, CHECK_OVF = false;
+  static constexpr bool F8 = false, SAT_CHECK = false, INF_CHECK = false;
   static constexpr float PMAX = 3.0e38f;
 };
 template <>
 struct InTraits<FS_F16> {
   static constexpr int EB = 2, KSTEP = 16;
   static constexpr uint32_t FMT = 0;
-  static constexpr bool F8 = false, CHECK_OVF = true;
+  // P overflow rounds to inf, which makes every element of the row's O non-finite: the
+  // epilogue checks O (free) instead of the norm warps checking every score
+  static constexpr bool F8 = false, SAT_CHECK = false, INF_CHECK = !FS_NO_OVF;
   static constexpr float PMAX = 65504.0f;
 };
 template <>
 struct InTraits<FS_E4M3> {
   static constexpr int EB = 1, KSTEP = 32;
   static constexpr uint32_t FMT = 0;
-  static constexpr bool F8 = true, CHECK_OVF = true;
-  static constexpr float PMAX = 448.0f;
+  // e4m3 conversion saturates (satfinite) instead of producing inf: the norm warps look for
+  // saturated codes (|p| rounded to 448, i.e. |p_scale s| >= 432) in chunks whose sum of a2(s)
+  // could reach that range
+  static constexpr bool F8 = true, SAT_CHECK = true, INF_CHECK = false;
+  static constexpr float PMAX = 432.0f;
 };
 
 template <int IN, int D, bool KS = false>
@@ -576,16 +584,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           za = __fadd2_rn(za, h0);
           zb = __fadd2_rn(zb, h1);
-          if constexpr (TR::CHECK_OVF) {
-            // max|s| <= sqrt(sum s^2) (<= sum |s|): only a chunk whose sum reaches ovf_z can overflow P
-            const float zh = (h0.x + h0.y) + (h1.x + h1.y);
-            if (zh >= p.ovf_z) {
-              float amax = 0.f;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(__uint_as_float(s[i])));
-              if (amax * fabsf(ps) > TR::PMAX) ovf = true;
-            }
-          }
+          // max|s| <= sqrt(sum s^2) (<= sum |s|): only a chunk whose sum reaches ovf_z can saturate P
+          const float zh = (h0.x + h0.y) + (h1.x + h1.y);
           // pack P (s[i] is written only after s[2i], s[2i+1] / s[4i..4i+3] are read)
           uint32_t pk[16];
           if constexpr (TR::F8) {
@@ -613,6 +613,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tmem_st8(s_addr + ch * 8, pk);
           else
             ptx::tmem_st16(s_addr + ch * 16, pk);
+          if constexpr (TR::SAT_CHECK) {
+            if (zh >= p.ovf_z) {  // rare: look for saturated e4m3 codes 0x7e / 0xfe (+-448)
+              uint32_t sat = 0;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const uint32_t t = (pk[i] & 0x7f7f7f7fu) ^ 0x7e7e7e7eu;  // zero byte <=> saturated
+                sat |= (t - 0x01010101u) & ~t & 0x80808080u;
+              }
+              if (sat) ovf = true;
+            }
+          }
           if (ch == 0) ptx::tmem_wait_ld();
         }
         ptx::tmem_wait_st();
@@ -662,18 +673,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool live = row < p.seqlen_q;
         const bool partial = p.part_num != nullptr;
         const float den = NORM == FS_NORM_SIGNED_L1 ? zr + p.eps : sqrtf(zr + p.eps);
-        const bool bad = !partial && (!(den > 0.f) || isinf(den));
         // partial mode: the unnormalised numerator (the combine step divides by b(sum z + eps))
-        const float mul = partial ? p.out_mul : __fdiv_rn(p.out_mul, den);
+        float mul = partial ? p.out_mul : __fdiv_rn(p.out_mul, den);
         // partial row index: ((split * B + batch) * H + head) * Nq + row
         const int64_t prow =
             ((static_cast<int64_t>(tc.split) * p.n_batch + tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
-        if (partial && live) p.part_z[prow] = zr;
-        if (live && bad && p.bad_key != nullptr) {
-          const uint64_t lin = (static_cast<uint64_t>(tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
-          atomicMin(reinterpret_cast<unsigned long long*>(p.bad_key),
-                    static_cast<unsigned long long>((lin << 32) | __float_as_uint(zr)));
-        }
+        // row status once O's first columns are in: FP16 P overflow (inf) makes every O element
+        // non-finite, so one column tells; it is reported as z = +inf like a saturated FP8 P
+        auto finish_row = [&](bool ovf_o) {
+          const float z_report = ovf_o ? __int_as_float(0x7f800000) : zr;
+          const bool bad = !partial && (ovf_o || !(den > 0.f) || isinf(den));
+          if (partial && live) p.part_z[prow] = z_report;
+          if (live && bad && p.bad_key != nullptr) {
+            const uint64_t lin = (static_cast<uint64_t>(tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
+            atomicMin(reinterpret_cast<unsigned long long*>(p.bad_key),
+                      static_cast<unsigned long long>((lin << 32) | __float_as_uint(z_report)));
+          }
+          if (ovf_o) mul = 0.f;  // flagged row: zeros rather than inf/NaN
+        };
         OT* dst = reinterpret_cast<OT*>(p.o) + tc.batch * p.o_sb + static_cast<int64_t>(row) * p.o_sn +
                   tc.head * p.o_sh;
         const uint32_t o_addr = tmem + lane_off + C::COL_O0 + (ob * NQT + t) * D;
@@ -697,8 +714,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] = 0u;
           }
+          if (c == 0) {
+            const float a0 = __uint_as_float(acc[0]);
+            finish_row(TR::INF_CHECK && !isfinite(a0) && isfinite(zr));
+          }
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(acc[i]) * mul;
+          for (int i = 0; i < 32; ++i) v[i] = (mul == 0.f) ? 0.f : __uint_as_float(acc[i]) * mul;
           if (partial) {
             if (live) store32<FS_F32>(p.part_num + prow * D + c * 32, v, c * 32, D);
           } else if (live && c * 32 < p.head_dim) {

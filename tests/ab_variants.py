@@ -26,6 +26,8 @@ AB_DIR = os.path.join(ROOT, "paper_2505_09326_b200", "_lib", "ab")
 
 CASES = {  # name: (B, N, H, D, dtype, eps)
     "c2": (16, 4096, 16, 64, "fp16", 0.0),
+    "c2b": (16, 4096, 16, 64, "bf16", 0.0),
+    "c5h": (64, 20000, 8, 64, "fp16", 1e-6),
     "c3": (8, 16384, 16, 128, "bf16", 0.0),
     "c4": (8, 8192, 16, 128, "e4m3", 0.0),
     "c5": (64, 20000, 8, 64, "bf16", 1e-6),
