@@ -66,7 +66,12 @@ __device__ unsigned long long g_prof[16];
 #endif
 
 constexpr int BM = 128;  // query rows per Q tile (= TMEM lanes)
-constexpr int BN = 128;  // keys per K/V tile
+#ifndef FS_BN192
+#define FS_BN192 1  // d=64 16-bit: 192-key K/V tiles (1.5x the work per ring / barrier round trip)
+#endif
+// keys per K/V tile: 192 for d=64 16-bit (S 2 x 192 + O 2 x 64 = 512 TMEM columns), else 128
+__host__ __device__ constexpr int bn_for(int in, int d) { return (FS_BN192 && in != FS_E4M3 && d == 64) ? 192 : 128; }
+constexpr int BN = 128;  // the default K/V tile (kernels use Cfg::BN)
 constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_NWT
 #define FS_NWT 8  // norm warps per Q tile: 8 (one per lane quarter x column half) or 4
@@ -79,6 +84,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #endif
 #ifndef FS_STAGES32
 #define FS_STAGES32 4  // K/V ring depth for 32 KB slots (d=128 16-bit); 5 fits without multiplicities but measured equal
+#endif
+#ifndef FS_KV1_MIN
+#define FS_KV1_MIN 6  // smallest ring (slots) that pairs K_j and V_j on one barrier
 #endif
 #ifndef FS_STAGES16
 #define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=64 16-bit, d=128 e4m3)
@@ -148,17 +156,20 @@ struct Cfg {
   static_assert(ROW_BYTES % 128 == 0, "head_dim * elem_bytes must be a multiple of 128 B (SW128)");
   static constexpr int NDB = ROW_BYTES / 128;  // 128-byte column blocks per row
   static constexpr int BOXW = 128 / EB;        // elements per TMA box row
+  static constexpr int BN = bn_for(IN, D);
   static constexpr int Q_TILE_BYTES = BM * ROW_BYTES;
   static constexpr int SLOT_BYTES = BN * ROW_BYTES;
-  // 32 KB slots (d=128, 16-bit): one Q buffer per tile, 4 ring slots.  16 KB slots (d=64 16-bit,
-  // d=128 e4m3): Q double-buffered (the next work tile's Q lands during this one), 8 ring slots.
+  // 32 KB slots (d=128, 16-bit): one Q buffer per tile, 4 ring slots.  16 KB slots (d=128 e4m3):
+  // Q double-buffered (the next work tile's Q lands during this one), 8 ring slots.  24 KB slots
+  // (d=64 16-bit, 192 keys): double-buffered Q, 6 ring slots.
   static constexpr int NQB = (SLOT_BYTES >= 32768) ? 1 : 2;
   // (32 KB slots: a fifth slot fits when no per-key multiplicity ring is needed and the dynamic
   //  shared-memory base is 1024-aligned -- checked on the device, see SLACK)
-  static constexpr int STAGES = (SLOT_BYTES >= 32768) ? (KS ? 4 : FS_STAGES32) : FS_STAGES16;
+  static constexpr int STAGES = (SLOT_BYTES >= 32768) ? (KS ? 4 : FS_STAGES32)
+                                : (SLOT_BYTES > 16384 ? 6 : FS_STAGES16);
   // K_j and V_j share one ring barrier when the ring is deep (8 slots): one wait per K/V tile on
   // the MMA issuer.  With 4 slots the pair would halve the prefetch distance (measured -10 % at C3).
-  static constexpr bool KV1 = FS_KV1 && STAGES >= 8;
+  static constexpr bool KV1 = FS_KV1 && STAGES >= FS_KV1_MIN;
   __device__ static uint32_t kv_bar(uint32_t slot) { return KV1 ? (slot & ~1u) : slot; }
   static constexpr int RING_OFF = NQT * NQB * Q_TILE_BYTES;
   static constexpr int BAR_OFF = RING_OFF + STAGES * SLOT_BYTES;
@@ -279,6 +290,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                          const KParams p) {
   using C = Cfg<IN, D, KS>;
   using TR = InTraits<IN>;
+  constexpr int BN = C::BN;  // keys per K/V tile for this configuration
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_s = ptx::smem_u32(smem_raw);
   if (C::SLACK == 0 && (raw_s & 1023u) != 0) __trap();  // layout needs an aligned base (see Cfg::SLACK)
@@ -549,13 +561,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int hi = 0; hi < NH; ++hi) {
         const int hh = hh0 + hi;
         const uint32_t s_addr = s_base + hh * (BN / 2);
-        // 64 columns in two 32-column chunks (80 registers/thread at 768 threads): chunk 1's TMEM
-        // load is issued once chunk 0 is packed, and overlaps chunk 0's P store.
+        // BN/2 columns in 32-column chunks (80 registers/thread at 768 threads): the next chunk's
+        // TMEM load is issued once this chunk is packed, and overlaps this chunk's P store.
+        constexpr int NCH = BN / 64;
         uint32_t s[32];
         ptx::tmem_ld32(s_addr, s);
         ptx::tmem_wait_ld();
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+        for (int ch = 0; ch < NCH; ++ch) {
           // sum of a2(s): packed FP32 FMAs / adds, two independent chains.  With KS the scores are
           // first scaled by the key multiplicities, s_ij <- m_j s_ij (fp32; exact for integer m).
           const float4* mp = reinterpret_cast<const float4*>(smem + C::MS_OFF + v_slot * C::MS_SLOT_BYTES) +
@@ -608,7 +621,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < 16; ++i)
               pk[i] = pack2<IN>(ps * __uint_as_float(s[2 * i]), ps * __uint_as_float(s[2 * i + 1]));
           }
-          if (ch == 0) ptx::tmem_ld32(s_addr + 32, s);  // chunk 1 (reuses s: chunk 0 is consumed)
+          if (ch + 1 < NCH) ptx::tmem_ld32(s_addr + 32 * (ch + 1), s);  // next chunk (s is consumed)
           if constexpr (TR::F8)
             ptx::tmem_st8(s_addr + ch * 8, pk);
           else
@@ -624,7 +637,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (sat) ovf = true;
             }
           }
-          if (ch == 0) ptx::tmem_wait_ld();
+          if (ch + 1 < NCH) ptx::tmem_wait_ld();
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
@@ -761,7 +774,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 static bool encode_bshd(CUtensorMap* map, CUtensorMapDataType dt, int eb, const void* ptr, int head_dim, int seqlen,
-                        int heads, int batch, const int64_t* stride, int box_w, std::string* err) {
+                        int heads, int batch, const int64_t* stride, int box_w, int box_rows, std::string* err) {
   auto enc = get_encode_fn();
   if (!enc) {
     *err = "cuTensorMapEncodeTiled unavailable (driver too old?)";
@@ -771,7 +784,7 @@ static bool encode_bshd(CUtensorMap* map, CUtensorMapDataType dt, int eb, const 
                         (cuuint64_t)batch};
   cuuint64_t strides[3] = {(cuuint64_t)(stride[1] * eb), (cuuint64_t)(stride[2] * eb),
                            (cuuint64_t)(stride[0] * eb)};
-  cuuint32_t box[4] = {(cuuint32_t)box_w, (cuuint32_t)BM, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)box_w, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, dt, 4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -781,6 +794,9 @@ static bool encode_bshd(CUtensorMap* map, CUtensorMapDataType dt, int eb, const 
   }
   return true;
 }
+
+static int kernel_d(const fs_fwd_params* p) { return (p->in_dtype == FS_E4M3 || p->head_dim > 64) ? 128 : 64; }
+static int kernel_bn(const fs_fwd_params* p) { return bn_for(p->in_dtype, kernel_d(p)); }
 
 // Key multiplicities m [batch, seqlen_kv] fp32 (token stride 1): 128-key boxes, zero-filled past
 // seqlen_kv so padded keys stay exactly zero.
@@ -793,7 +809,7 @@ static bool encode_key_scale(CUtensorMap* map, const fs_fwd_params* p, std::stri
   cuuint64_t dims[2] = {(cuuint64_t)(p->seqlen_kv > 0 ? p->seqlen_kv : 1), (cuuint64_t)p->batch};
   const int64_t sb = p->batch > 1 ? p->key_scale_stride : ((p->seqlen_kv + 3) / 4) * 4;
   cuuint64_t strides[1] = {(cuuint64_t)(sb * 4)};
-  cuuint32_t box[2] = {(cuuint32_t)BN, 1};
+  cuuint32_t box[2] = {(cuuint32_t)kernel_bn(p), 1};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p->key_scale), dims, strides, box,
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -828,14 +844,15 @@ struct SplitPlan {
 };
 static SplitPlan split_plan(const fs_fwd_params* p) {
   SplitPlan sp;
-  sp.n_kv_tiles = (p->seqlen_kv + BN - 1) / BN;
+  const int bn = kernel_bn(p);
+  sp.n_kv_tiles = (p->seqlen_kv + bn - 1) / bn;
   int s = std::max(1, p->kv_splits);
   s = std::max(1, std::min(s, sp.n_kv_tiles));
   sp.split_tiles = sp.n_kv_tiles > 0 ? (sp.n_kv_tiles + s - 1) / s : 0;
   sp.splits = sp.split_tiles > 0 ? (sp.n_kv_tiles + sp.split_tiles - 1) / sp.split_tiles : 1;
   return sp;
 }
-static int kernel_d(const fs_fwd_params* p) { return (p->in_dtype == FS_E4M3 || p->head_dim > 64) ? 128 : 64; }
+
 
 // Merge of K/V-range partials (streaming.py:122-128, Lemma 1: (o, z) add, no
 // rescale): O = sum_s num_s / b(sum_s z_s + eps), plus the bad-row key.  One thread per 4 columns.
@@ -934,11 +951,12 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
                                                   : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   CUtensorMap tq, tk, tv;
   std::string err;
-  if (!encode_bshd(&tq, dt, C::EB, p->q, p->head_dim, p->seqlen_q, p->heads_q, p->batch, p->q_stride, C::BOXW, &err) ||
-      !encode_bshd(&tk, dt, C::EB, p->k, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->k_stride, C::BOXW,
+  if (!encode_bshd(&tq, dt, C::EB, p->q, p->head_dim, p->seqlen_q, p->heads_q, p->batch, p->q_stride, C::BOXW, BM,
                    &err) ||
+      !encode_bshd(&tk, dt, C::EB, p->k, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->k_stride, C::BOXW,
+                   C::BN, &err) ||
       !encode_bshd(&tv, dt, C::EB, p->v, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->v_stride, C::BOXW,
-                   &err))
+                   C::BN, &err))
     return fail(FS_ERR_UNSUPPORTED, err);
   CUtensorMap tm = tq;  // unused unless KS
   if (KS && !encode_key_scale(&tm, p, &err)) return fail(FS_ERR_UNSUPPORTED, err);
@@ -1062,7 +1080,7 @@ int fs_query_tile(int head_dim, fs_dtype dt, int* bm, int* bn) {
   if (!bm || !bn || head_dim < 1 || head_dim > 128) return 1;
   if (dt != FS_F16 && dt != FS_BF16 && dt != FS_E4M3) return 1;
   *bm = fs::BM;
-  *bn = fs::BN;
+  *bn = fs::bn_for(dt, (dt == FS_E4M3 || head_dim > 64) ? 128 : 64);
   return 0;
 }
 

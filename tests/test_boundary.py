@@ -102,7 +102,8 @@ def test_fs_fwd_validation(kw, status, needle):
 
 
 def test_query_tile():
-    assert _lib.query_tile(64, _lib.FS_BF16) == (128, 128)
+    assert _lib.query_tile(64, _lib.FS_BF16) == (128, 192)   # d=64 16-bit: 192-key K/V tiles
+    assert _lib.query_tile(128, _lib.FS_BF16) == (128, 128)
     assert _lib.query_tile(128, _lib.FS_E4M3) == (128, 128)
     with pytest.raises(ValueError):
         _lib.query_tile(0, _lib.FS_BF16)

@@ -384,7 +384,8 @@ def test_compat_meter_records_kernel_tile():
         m = at.ScoreBufferMeter()
         at.streamed_attention_array(rng.standard_normal((y, 64)), rng.standard_normal((x, 64)),
                                     rng.standard_normal((x, 64)), SPHERICAL, 1.0, at.TileConfig(8, 8), meter=m)
-        assert m.peak_elements == min(128, y) * min(128, x)
+        bm, bn = __import__("paper_2505_09326_b200")._lib.query_tile(64, 1)  # the kernel's tile (d=64)
+        assert m.peak_elements == min(bm, y) * min(bn, x)
 
 
 def test_compat_empty_query_returns_empty():
