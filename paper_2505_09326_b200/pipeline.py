@@ -28,20 +28,28 @@ class HostPipeline:
                                    (device if isinstance(device, int) else device.index))
         self.chunk = chunk
         self.q_split = q_split
+        self._sms = None
         self._shape_key = None
         self.s_in = torch.cuda.Stream(self.device)
         self.s_cmp = torch.cuda.Stream(self.device)
         self.s_out = torch.cuda.Stream(self.device)
 
-    def _slices(self, nq: int) -> list[tuple[int, int]]:
-        # query slices of >= 1024 rows (4 work tiles per head), at most 4 per batch chunk
-        qs = self.q_split if self.q_split is not None else max(1, min(4, nq // 1024))
+    def _slices(self, nq: int, heads: int = 1) -> list[tuple[int, int]]:
+        # Query slices: as many as keep >= 3 full waves of work tiles per launch (at most 4), so
+        # slicing shortens the pipeline's fill/drain without leaving SMs idle in a launch's tail.
+        if self.q_split is not None:
+            qs = self.q_split
+        else:
+            if self._sms is None:
+                self._sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            tiles = self.chunk * heads * -(-nq // 256)
+            qs = max(1, min(4, tiles // (3 * self._sms)))
         step = -(-nq // qs)
         step = -(-step // 256) * 256  # whole 256-row work tiles
         return [(n0, min(nq, n0 + step)) for n0 in range(0, nq, step)] or [(0, 0)]
 
     def _alloc(self, q, k, out, key_scale=None):
-        sl = self._slices(q.shape[1])
+        sl = self._slices(q.shape[1], q.shape[2])
         qmax = max(b - a for a, b in sl)
         key = (tuple(q.shape[1:]), tuple(k.shape[1:]), q.dtype, out.dtype, self.chunk, qmax,
                None if key_scale is None else tuple(key_scale.shape[1:]))
@@ -69,7 +77,7 @@ class HostPipeline:
         self._alloc(q, k, out, key_scale)
         c = self.chunk
         nb, nq, h = q.shape[0], q.shape[1], q.shape[2]
-        slices = self._slices(nq)
+        slices = self._slices(nq, h)
         ev_q_free = [None, None]     # compute done with Q slot / O slot producer side
         ev_o_free = [None, None]     # D2H of O slot done
         ev_kv_free = [None, None]    # last compute of a batch chunk done with its K/V slot
