@@ -208,3 +208,31 @@ def test_product_never_imports_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|\"\"\".*?\"\"\"", "", src, flags=re.S).replace(
                     "oracle/", ""), f"{f} references the oracle"
+
+
+def test_split_plan_host_functions():
+    # fs_kv_splits / fs_partial_floats are host-only: effective splits clamp to [1, K/V tiles] and
+    # leave no empty range; the workspace holds S x rows x (Dk + 1) floats
+    lib = _lib.load()
+    p = _params(head_dim=128, seqlen_kv=1000, seqlen_q=300, batch=2, heads_q=4, heads_kv=2)
+    for req in (0, 1, 2, 3, 7, 100):
+        p.kv_splits = req
+        got = lib.fs_kv_splits(ctypes.byref(p))
+        assert 1 <= got <= 8 and (req <= 1 and got == 1 or req > 1)
+    p.kv_splits = 7   # 8 tiles of 128 keys, ceil(8/7)=2 per split -> 4 non-empty splits
+    assert lib.fs_kv_splits(ctypes.byref(p)) == 4
+    assert lib.fs_partial_floats(ctypes.byref(p)) == 4 * 2 * 4 * 300 * (128 + 1)
+    p.head_dim, p.in_dtype = 64, _lib.FS_BF16   # d=64 16-bit: 192-key tiles -> 6 tiles
+    p.kv_splits = 100
+    assert lib.fs_kv_splits(ctypes.byref(p)) == 6
+    assert lib.fs_partial_floats(ctypes.byref(p)) == 6 * 2 * 4 * 300 * (64 + 1)
+    p.kv_splits, p.partial = 2, None
+    assert lib.fs_fwd(ctypes.byref(p), None) == _lib.FS_ERR_CONFIG and "partial" in _lib.last_error()
+
+
+def test_auto_splits_wave_model():
+    import paper_2505_09326_b200.flashsign as fsm
+    fsm._SMS[0] = 148
+    assert fsm.auto_splits(8, 16, 16384, 16384, "cuda:0", 128) == 1       # C3: 8192 tiles
+    assert fsm.auto_splits(1, 1, 16384, 16384, "cuda:0", 128) > 1         # 64 tiles on 148 SMs
+    assert fsm.auto_splits(1, 1, 300, 700, "cuda:0", 128) == 1            # too few K/V tiles (6)

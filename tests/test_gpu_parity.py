@@ -703,3 +703,50 @@ def test_16bit_descales_and_p_scale(dt):
                  out_dtype=torch.float32)
     ref = oracle_of(q.float() * 2.0, k.float() * 0.5, v.float() * 4.0, 0.5)
     check_tol(o.cpu().numpy() / 4.0, ref / 4.0, dt, f"{dt} descales")
+
+
+# ------------------------------------------------------------------ randomized sweep over the feature matrix
+
+def _sweep_cases(n=48, seed=2024):
+    rng = np.random.default_rng(seed)
+    dts = [torch.bfloat16, torch.float16, torch.float8_e4m3fn]
+    out = []
+    for i in range(n):
+        dt = dts[i % 3]
+        d = int(rng.choice([16, 32, 48, 64, 80, 96, 112, 128] if dt != torch.float8_e4m3fn else [16, 32, 64, 96, 128]))
+        hkv = int(rng.choice([1, 2, 3]))
+        h = hkv * int(rng.choice([1, 2, 4]))
+        out.append(dict(dt=dt, b=int(rng.integers(1, 4)), nq=int(rng.integers(1, 700)), nkv=int(rng.integers(1, 900)),
+                        h=h, hkv=hkv, d=d, norm=str(rng.choice(["spherical", "signed_l1"])),
+                        ks=bool(rng.integers(0, 2)), splits=int(rng.choice([1, 1, 2, 3])),
+                        scale=float(rng.choice([1.0, -0.5, 2.0])), eps=float(rng.choice([0.0, 1e-3])),
+                        out=[torch.float32, torch.bfloat16][int(rng.integers(0, 2))], seed=int(rng.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"{str(c['dt'])[6:]}-d{c['d']}-n{c['nq']}x{c['nkv']}-"
+                                                                f"h{c['h']}/{c['hkv']}-{c['norm']}-ks{int(c['ks'])}-s{c['splits']}")
+def test_random_feature_sweep(case):
+    c = case
+    g = torch.Generator(device="cuda").manual_seed(c["seed"])
+    q = torch.randn((c["b"], c["nq"], c["h"], c["d"]), generator=g, device="cuda").to(c["dt"])
+    k = torch.randn((c["b"], c["nkv"], c["hkv"], c["d"]), generator=g, device="cuda").to(c["dt"])
+    v = torch.randn((c["b"], c["nkv"], c["hkv"], c["d"]), generator=g, device="cuda").to(c["dt"])
+    m = torch.randint(0, 4, (c["b"], c["nkv"]), generator=g, device="cuda").float() if c["ks"] else None
+    eps = c["eps"] if not c["ks"] else max(c["eps"], 1e-3)  # zero multiplicities can empty a row
+    o = fs().fwd(q, k, v, scale=c["scale"], eps=eps, out_dtype=c["out"], normalizer=c["norm"], key_scale=m,
+                 kv_splits=c["splits"], check=False)
+    ref = exact_of(q, k, v, c["scale"], eps, c["norm"], m)
+    got = o.float().cpu().numpy()
+    finite = np.isfinite(ref).all(axis=-1)
+    assert finite.mean() > 0.5
+    got, ref = got[finite], ref[finite]
+    err = np.abs(got - ref)
+    scale_ref = np.abs(ref).max()
+    # per-dtype tolerance relative to the output scale (the input dtype's rounding dominates)
+    tol = {torch.float16: 0.01, torch.bfloat16: 0.05, torch.float8_e4m3fn: 0.35}[c["dt"]]
+    if c["out"] == torch.bfloat16:
+        tol = max(tol, 0.02)
+    assert err.max() <= tol * max(scale_ref, 1e-3) + 1e-6, (c, float(err.max()), float(scale_ref))
+    rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+    assert rel <= {torch.float16: 4e-3, torch.bfloat16: 1.5e-2, torch.float8_e4m3fn: 8e-2}[c["dt"]], (c, rel)
