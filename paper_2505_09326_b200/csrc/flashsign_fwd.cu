@@ -77,7 +77,7 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #define FS_NWT 8  // norm warps per Q tile: 8 (one per lane quarter x column half) or 4
 #endif
 #ifndef FS_KV1
-#define FS_KV1 1  // K_j and V_j share one ring barrier when the ring has 8 slots (see Cfg::KV1)
+#define FS_KV1 1  // K_j and V_j share one ring barrier when the ring has >= FS_KV1_MIN slots (Cfg::KV1)
 #endif
 #ifndef FS_NO_OVF
 #define FS_NO_OVF 0  // experiment knob: skip the fp16 P-overflow check
@@ -89,7 +89,7 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #define FS_KV1_MIN 6  // smallest ring (slots) that pairs K_j and V_j on one barrier
 #endif
 #ifndef FS_STAGES16
-#define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=64 16-bit, d=128 e4m3)
+#define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=128 e4m3)
 #endif
 constexpr int NWT = FS_NWT;
 static_assert(NWT == 4 || NWT == 8, "norm warps per Q tile");
