@@ -80,7 +80,7 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #define FS_KV1 1  // K_j and V_j share one ring barrier when the ring has >= FS_KV1_MIN slots (Cfg::KV1)
 #endif
 #ifndef FS_NO_OVF
-#define FS_NO_OVF 0  // experiment knob: skip the fp16 P-overflow check
+#define FS_NO_OVF 0  // experiment knob: skip the FP16 / FP8 P-range checks
 #endif
 #ifndef FS_STAGES32
 #define FS_STAGES32 4  // K/V ring depth for 32 KB slots (d=128 16-bit); 5 fits without multiplicities but measured equal
@@ -144,7 +144,7 @@ struct InTraits<FS_E4M3> {
   // e4m3 conversion saturates (satfinite) instead of producing inf: the norm warps look for
   // saturated codes (|p| rounded to 448, i.e. |p_scale s| >= 432) in chunks whose sum of a2(s)
   // could reach that range
-  static constexpr bool F8 = true, SAT_CHECK = true, INF_CHECK = false;
+  static constexpr bool F8 = true, SAT_CHECK = !FS_NO_OVF, INF_CHECK = false;
   static constexpr float PMAX = 432.0f;
 };
 
@@ -567,13 +567,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t s[32];
         ptx::tmem_ld32(s_addr, s);
         ptx::tmem_wait_ld();
+        // FP8: every chunk's packed codes and the half's sum of a2(s), for one saturation check per
+        // half after its last store (off the chunk-to-chunk path)
+        uint32_t pk8[TR::SAT_CHECK ? NCH * 8 : 1];
+        // sum of a2(s) over this half: packed FP32 FMAs / adds, two independent chains
+        float2 h0 = make_float2(0.f, 0.f), h1 = h0;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
-          // sum of a2(s): packed FP32 FMAs / adds, two independent chains.  With KS the scores are
+          // (a2(s) accumulates into the half's h0 / h1 chains)  With KS the scores are
           // first scaled by the key multiplicities, s_ij <- m_j s_ij (fp32; exact for integer m).
           const float4* mp = reinterpret_cast<const float4*>(smem + C::MS_OFF + v_slot * C::MS_SLOT_BYTES) +
                              (hh * (BN / 2) + ch * 32) / 4;
-          float2 h0 = make_float2(0.f, 0.f), h1 = h0;
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             float2 a = make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1]));
@@ -595,12 +599,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               h1 = __ffma2_rn(b, b, h1);
             }
           }
-          za = __fadd2_rn(za, h0);
-          zb = __fadd2_rn(zb, h1);
-          // max|s| <= sqrt(sum s^2) (<= sum |s|): only a chunk whose sum reaches ovf_z can saturate P
-          const float zh = (h0.x + h0.y) + (h1.x + h1.y);
           // pack P (s[i] is written only after s[2i], s[2i+1] / s[4i..4i+3] are read)
-          uint32_t pk[16];
+          uint32_t pk_local[16];
+          uint32_t* pk = TR::SAT_CHECK ? pk8 + (TR::SAT_CHECK ? ch * 8 : 0) : pk_local;
           if constexpr (TR::F8) {
             if (ps == 1.0f) {
 #pragma unroll
@@ -626,18 +627,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tmem_st8(s_addr + ch * 8, pk);
           else
             ptx::tmem_st16(s_addr + ch * 16, pk);
-          if constexpr (TR::SAT_CHECK) {
-            if (zh >= p.ovf_z) {  // rare: look for saturated e4m3 codes 0x7e / 0xfe (+-448)
-              uint32_t sat = 0;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const uint32_t t = (pk[i] & 0x7f7f7f7fu) ^ 0x7e7e7e7eu;  // zero byte <=> saturated
-                sat |= (t - 0x01010101u) & ~t & 0x80808080u;
-              }
-              if (sat) ovf = true;
-            }
-          }
           if (ch + 1 < NCH) ptx::tmem_wait_ld();
+        }
+        za = __fadd2_rn(za, h0);
+        zb = __fadd2_rn(zb, h1);
+        if constexpr (TR::SAT_CHECK) {
+          // max|s| <= sqrt(sum s^2) (<= sum |s|): only a half whose sum reaches ovf_z can hold a
+          // saturated code; then look for 0x7e / 0xfe (+-448) in its packed P
+          if ((h0.x + h0.y) + (h1.x + h1.y) >= p.ovf_z) {
+            uint32_t sat = 0;
+#pragma unroll
+            for (int i = 0; i < NCH * 8; ++i) {
+              const uint32_t tt = (pk8[i] & 0x7f7f7f7fu) ^ 0x7e7e7e7eu;  // zero byte <=> saturated
+              sat |= (tt - 0x01010101u) & ~tt & 0x80808080u;
+            }
+            if (sat) ovf = true;
+          }
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
