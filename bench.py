@@ -190,10 +190,25 @@ def cpu_reference_sample(cfg, rows: int, seed: int = 7):
     return dt, 4.0 * rows * N * D, threads or os.cpu_count()
 
 
+def _all_host_threads():
+    """BLAS thread pool sized to every host core (torchrun sets OMP_NUM_THREADS=1 per rank)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=os.cpu_count(), user_api="blas")
+    except Exception:
+        import contextlib
+        return contextlib.nullcontext()
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # reference arm: rank 0 only
+    with _all_host_threads():
+        _run_reference(args, cfg)
+
+
+def _run_reference(args, cfg):
     rows = args.ref_rows
     times = []
     for i in range(args.warmup + args.steps):
@@ -268,10 +283,18 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    # FS_BENCH_BACKEND=gloo runs the multi-rank path on a box with fewer GPUs than ranks (ranks
+    # share devices round-robin) -- a functional check of the sharded bench, not a measurement
+    backend = os.environ.get("FS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     B, H, HKV, N, D = cfg["B"], cfg["H"], cfg["HKV"], cfg["N"], cfg["D"]
     n_units = B * HKV
@@ -379,7 +402,8 @@ def run_ours(args, cfg):
         cpu = None
         if world == 1 and not args.no_cpu:
             rows = args.cpu_rows or N
-            dt, fl, threads = cpu_reference_sample(cfg, rows)
+            with _all_host_threads():
+                dt, fl, threads = cpu_reference_sample(cfg, rows)
             cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
                    "sample": f"{rows} query rows x {N} keys x d{D}, one (b,h) slice, float32, tile 64x64 "
                              f"(oracle port of attention.py:146-200), {dt:.2f} s",
