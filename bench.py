@@ -341,6 +341,26 @@ def run_ours(args, cfg):
     value = total_flops / (ms_step * 1e-3) / 1e12 if world > 1 else my_flops / (ms_step * 1e-3) / 1e12
     kernel_ms = ms_step / n_launch_per_step  # one kernel launch per piece; back-to-back on one stream
 
+    # ---------------- optional O gather onto every rank (NCCL all_gather), timed separately
+    gather = None
+    if world > 1 and n_units % world == 0 and ((hi - lo) % HKV == 0) and lo % HKV == 0:
+        o_mine = o[(lo - u_off) // HKV:(hi - u_off) // HKV]
+        for _ in range(2):
+            partition.gather_output(o_mine)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(3):
+            full = partition.gather_output(o_mine)
+        g1.record()
+        torch.cuda.synchronize()
+        tg = torch.tensor([g0.elapsed_time(g1) / 3], device=dev, dtype=torch.float64)
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        gather = {"ms": float(tg.item()), "bytes_per_rank_out": int(full.numel() * full.element_size()),
+                  "api": "partition.gather_output (all_gather_into_tensor)", "in_timed_region": False}
+        del full
+
     # ---------------- end-to-end through the host-buffer API (pinned host in, host out)
     e2e = None
     if not args.no_e2e:
@@ -420,7 +440,7 @@ def run_ours(args, cfg):
                        "l2": "inputs larger than L2 (no flush needed)",
                        "flops_per_step": total_flops},
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": n_launch_per_step * args.steps,
-            "roofline": roofline, "cpu_baseline": cpu,
+            "roofline": roofline, "cpu_baseline": cpu, "gather": gather,
         }
         if ctx is not None:
             line["context"] = ctx
