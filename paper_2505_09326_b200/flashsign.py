@@ -133,7 +133,7 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
                 or tuple(ks.shape) != (b, nkv) or (nkv > 0 and ks.stride(1) != 1)):
             raise ShapeMismatchError(f"flashsign: key_scale must be float32 [{b}, {nkv}] on {q.device} with unit "
                                      f"key stride, got {tuple(key_scale.shape)} {key_scale.dtype}")
-        if (b > 1 and (ks.stride(0) * 4) % 16 != 0) or ks.data_ptr() % 16 != 0:
+        if (b > 1 and ((ks.stride(0) * 4) % 16 != 0 or ks.stride(0) < nkv)) or ks.data_ptr() % 16 != 0:
             ks = _padded_rows(ks)
         prm.key_scale, prm.key_scale_stride = ks.data_ptr(), ks.stride(0)
         key_scale = ks  # keep alive until the launch is enqueued
@@ -153,6 +153,12 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
     if stream is None:
         with torch.cuda.device(q.device):
             stream = torch.cuda.current_stream()
+    else:
+        # buffers allocated here on the current stream but used on `stream`: keep the caching
+        # allocator from recycling them before `stream` is done with them
+        for t in (out, bad_key, partial, key_scale):
+            if t is not None:
+                t.record_stream(stream)
     st = lib.fs_fwd(ctypes.byref(prm), ctypes.c_void_p(stream.cuda_stream))
     if st != _lib.FS_OK:
         raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
