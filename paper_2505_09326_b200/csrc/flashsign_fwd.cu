@@ -88,6 +88,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_KV1_MIN
 #define FS_KV1_MIN 6  // smallest ring (slots) that pairs K_j and V_j on one barrier
 #endif
+#ifndef FS_TMA_ONCE
+#define FS_TMA_ONCE 0  // experiment (wrong results): stream K/V once, then reuse the stale ring
+#endif
 #ifndef FS_STAGES16
 #define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=128 e4m3)
 #endif
@@ -392,6 +395,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t round = kv_i / C::STAGES;
           const bool with_m = KS && (i & 1);  // V slots also carry the tile's key multiplicities
           uint64_t* full = &bars->kv_full[C::kv_bar(slot)];
+          if (FS_TMA_ONCE && kv_i >= C::STAGES) {  // experiment: no K/V traffic after the first ring
+            if (!C::KV1 || !(i & 1)) {
+              ptx::mbar_wait(&bars->kv_empty[C::kv_bar(slot)], (round & 1u) ^ 1u);
+              ptx::mbar_arrive(full);
+            }
+            if (i == q_next_at && next < p.n_tiles) load_q(next, it + 1);
+            continue;
+          }
           if (!C::KV1 || !(i & 1)) {
             ptx::mbar_wait(&bars->kv_empty[C::kv_bar(slot)], (round & 1u) ^ 1u);
             // with KV1 the K load announces both tiles' bytes (V follows right after)

@@ -22,7 +22,13 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int n_groups, unsigned long 
   __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x / 32;
-  for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  // random bf16 operands (sign, exponent near 1, random mantissa): realistic multiplier toggling
+  for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) {
+    uint32_t x = (uint32_t)i * 2654435761u + blockIdx.x * 97u;
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    const uint32_t lo = 0x3f00u | (x & 0x807fu), hi = 0x3f00u | ((x >> 16) & 0x807fu);
+    reinterpret_cast<uint32_t*>(smem)[i] = lo | (hi << 16);
+  }
   if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); fence_barrier_init(); }
   if (warp == 1) tmem_alloc(&tbase, 512);
   fence_proxy_async();
