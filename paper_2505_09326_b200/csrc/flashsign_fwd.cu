@@ -91,10 +91,14 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_TMA_ONCE
 #define FS_TMA_ONCE 0  // experiment (wrong results): stream K/V once, then reuse the stale ring
 #endif
+#ifndef FS_MC
+#define FS_MC 1  // CTA pairs (clusters of 2) on adjacent query blocks: K/V tiles multicast, L2 reads halved
+#endif
 #ifndef FS_STAGES16
 #define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=128 e4m3)
 #endif
 constexpr int NWT = FS_NWT;
+constexpr int CL = FS_MC ? 2 : 1;  // CTAs per cluster (sharing every K/V tile)
 static_assert(NWT == 4 || NWT == 8, "norm warps per Q tile");
 constexpr int NUM_THREADS = 32 * (4 + 2 * NWT + 4);
 constexpr int TMEM_COLS = 512;
@@ -105,7 +109,7 @@ struct KParams {
   void* o;
   int64_t o_sb, o_sn, o_sh;
   int32_t heads_q, heads_kv, seqlen_q, seqlen_kv, head_dim;
-  int32_t n_qblk;   // work tiles per (batch, head) = ceil(seqlen_q / (NQT*BM))
+  int32_t n_qblk;   // work tiles per (batch, head, K/V range) = ceil(seqlen_q / (NQT*BM*CL))
   int32_t n_tiles;  // n_qblk * heads_q * batch
   float zmul;       // spherical: (scale*q_descale*k_descale)^2; signed L1: |scale*q_descale*k_descale|
   float out_mul;    // scale * q_descale * k_descale * v_descale / p_scale
@@ -277,9 +281,9 @@ __device__ __forceinline__ void store32(typename OutT<OUT>::T* dst, const float*
 struct TileCoord {
   int qblk, head, batch, split, kb0, L;  // K/V tiles [kb0, kb0 + L) of this work tile
 };
-__device__ __forceinline__ TileCoord decode_tile(int tile, const KParams& p) {
+__device__ __forceinline__ TileCoord decode_tile(int tile, const KParams& p, int rank) {
   TileCoord c;
-  c.qblk = tile % p.n_qblk;
+  c.qblk = (tile % p.n_qblk) * CL + rank;  // the CTAs of a cluster take adjacent query blocks
   const int rest = tile / p.n_qblk;
   c.split = rest % p.kv_splits;
   const int bh = rest / p.kv_splits;
@@ -311,6 +315,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_kv_tiles = (p.seqlen_kv + BN - 1) / BN;
+  // clusters of CL CTAs walk the work tiles together (same K/V stream, adjacent query blocks)
+  const int rank = CL > 1 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+  const int tile0 = static_cast<int>(blockIdx.x) / CL, tstride = static_cast<int>(gridDim.x) / CL;
 
   if (threadIdx.x == 32) {
 #pragma unroll
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&bars->kv_full[s], 1);
-      ptx::mbar_init(&bars->kv_empty[s], 1);
+      ptx::mbar_init(&bars->kv_empty[s], CL);  // both CTAs of a cluster consume every slot
     }
     ptx::fence_barrier_init();
     ptx::fence_proxy_async();
@@ -345,7 +352,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == 2) ptx::tmem_alloc(&bars->tmem_base, TMEM_COLS);
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CL > 1)
+    ptx::cluster_sync();  // the peer's barriers exist before anything is multicast into them
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
@@ -357,7 +367,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t kv_i = 0;  // loads issued into the ring so far (K and V alternate)
       // Q tiles of work tile `tile_` (the it_-th of this CTA) into buffer it_ % NQB once it is free
       auto load_q = [&](int tile_, int it_) {
-        const TileCoord qc = decode_tile(tile_, p);
+        const TileCoord qc = decode_tile(tile_, p, rank);
         const int qb = it_ % C::NQB;
         const uint32_t q_use = static_cast<uint32_t>(it_ / C::NQB);
 #pragma unroll
@@ -371,15 +381,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                              qc.batch, pol_q);
         }
       };
-      load_q(blockIdx.x, 0);
+      load_q(tile0, 0);
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
-        const TileCoord tc = decode_tile(tile, p);
+      for (int tile = tile0; tile < p.n_tiles; tile += tstride, ++it) {
+        const TileCoord tc = decode_tile(tile, p, rank);
         const int head_kv = static_cast<int>((static_cast<int64_t>(tc.head) * p.heads_kv) / p.heads_q);
-        const int next = tile + static_cast<int>(gridDim.x);
+        const int next = tile + tstride;
         if (C::NQB == 1 && next < p.n_tiles) {
           // single Q buffer: pull the next work tile's Q into L2 now so its reload is an L2 hit
-          const TileCoord nx = decode_tile(next, p);
+          const TileCoord nx = decode_tile(next, p, rank);
 #pragma unroll
           for (int t = 0; t < NQT; ++t)
 #pragma unroll
@@ -414,9 +424,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (with_m)
             ptx::tma_load_2d(smem + C::MS_OFF + slot * C::MS_SLOT_BYTES, &tm_m, full, key0, tc.batch, pol_kv);
 #pragma unroll
-          for (int db = 0; db < C::NDB; ++db)
-            ptx::tma_load_4d(smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128), tm, full,
-                             db * C::BOXW, key0, head_kv, tc.batch, pol_kv);
+          for (int db = 0; db < C::NDB; ++db) {
+            uint8_t* dst = smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128);
+            if constexpr (CL > 1)  // this CTA's rows of the tile, into both CTAs of the pair
+              ptx::tma_load_4d_mc(dst + rank * (BN / CL) * 128, tm, full, db * C::BOXW, key0 + rank * (BN / CL),
+                                  head_kv, tc.batch, static_cast<uint16_t>((1u << CL) - 1u), pol_kv);
+            else
+              ptx::tma_load_4d(dst, tm, full, db * C::BOXW, key0, head_kv, tc.batch, pol_kv);
+          }
           if (i == q_next_at && next < p.n_tiles) load_q(next, it + 1);
         }
       }
@@ -430,6 +445,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool leader = ptx::elect_one();
       // every lane runs the issue code; the elected lane's predicate makes it the only issuer
       const uint32_t lp = leader ? 1u : 0u;
+      // a ring slot is free once every CTA of the cluster has consumed it
+      auto kv_release = [&](uint64_t* bar) {
+        if constexpr (CL > 1)
+          ptx::tc_commit_mc_p(bar, static_cast<uint16_t>((1u << CL) - 1u), lp);
+        else
+          ptx::tc_commit_p(bar, lp);
+      };
       const uint64_t q_desc = ptx::sdesc_sw128(smem_s, 16, 1024);
       const uint64_t k_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, 16, 1024);
       const uint64_t v_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, BN * 128, 1024);
@@ -441,12 +463,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t kv_i = 0;                 // ring position of this work tile's K_0
       uint32_t p_use[NQT] = {0u, 0u};    // completed phases of p_full[t]
       int it = 0;
-      for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+      for (int tile = tile0; tile < p.n_tiles; tile += tstride, ++it) {
         const int qb = it % C::NQB;
         const uint32_t q_use = static_cast<uint32_t>(it / C::NQB);
         const int ob = it % C::NOB;
         const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
-        const int L = decode_tile(tile, p).L;
+        const int L = decode_tile(tile, p, rank).L;
         auto qk = [&](int t, uint32_t slot) {
           const uint64_t a0 = q_desc + static_cast<uint32_t>(((t * C::NQB + qb) * C::Q_TILE_BYTES) >> 4);
           const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
@@ -512,11 +534,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (j == L - 1) ptx::tc_commit_p(&bars->q_empty[0][qb], lp);
           if (j > 0) {
             pv(1, prev_v_slot, j - 1);
-            ptx::tc_commit_p(&bars->kv_empty[C::kv_bar(prev_v_slot)], lp);
+            kv_release(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
           }
           qk(1, k_slot);
           ptx::tc_commit_p(&bars->s_full[1], lp);
-          if (!C::KV1) ptx::tc_commit_p(&bars->kv_empty[k_slot], lp);  // KV1: freed with V after PV1
+          if (!C::KV1) kv_release(&bars->kv_empty[k_slot]);  // KV1: freed with V after PV1
           if (j == L - 1) ptx::tc_commit_p(&bars->q_empty[1][qb], lp);
           if (!C::KV1) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
           pv(0, v_slot, j);
@@ -524,7 +546,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           prev_v_slot = v_slot;
         }
         pv(1, prev_v_slot, L - 1);
-        ptx::tc_commit_p(&bars->kv_empty[C::kv_bar(prev_v_slot)], lp);
+        kv_release(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
         ptx::tc_commit_p(&bars->o_full[1][ob], lp);
         kv_i += 2 * L;
       }
@@ -552,11 +574,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     long long pr_sw = 0, pr_nc = 0, pr_nn = 0;
 #endif
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles && n_kv_tiles > 0; tile += gridDim.x, ++it) {
+    for (int tile = tile0; tile < p.n_tiles && n_kv_tiles > 0; tile += tstride, ++it) {
       const int ob = it % C::NOB;
       float2 za = make_float2(0.f, 0.f), zb = za;
       bool ovf = false;
-      const int L = decode_tile(tile, p).L;
+      const int L = decode_tile(tile, p, rank).L;
       for (int j = 0; j < L; ++j) {
 #if FS_PROF
         const long long tn0 = clock64();
@@ -689,8 +711,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     using OT = typename OutT<OUT>::T;
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
-      const TileCoord tc = decode_tile(tile, p);
+    for (int tile = tile0; tile < p.n_tiles; tile += tstride, ++it) {
+      const TileCoord tc = decode_tile(tile, p, rank);
       const int ob = it % C::NOB;
       const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
 #pragma unroll 1
@@ -771,6 +793,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, TMEM_COLS);
   }
+  if (CL > 1) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
 }
 
 // ====================================================================== host
@@ -976,9 +999,9 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   if (!encode_bshd(&tq, dt, C::EB, p->q, p->head_dim, p->seqlen_q, p->heads_q, p->batch, p->q_stride, C::BOXW, BM,
                    &err) ||
       !encode_bshd(&tk, dt, C::EB, p->k, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->k_stride, C::BOXW,
-                   C::BN, &err) ||
+                   C::BN / CL, &err) ||
       !encode_bshd(&tv, dt, C::EB, p->v, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->v_stride, C::BOXW,
-                   C::BN, &err))
+                   C::BN / CL, &err))
     return fail(FS_ERR_UNSUPPORTED, err);
   CUtensorMap tm = tq;  // unused unless KS
   if (KS && !encode_key_scale(&tm, p, &err)) return fail(FS_ERR_UNSUPPORTED, err);
@@ -1002,7 +1025,7 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   const double pmax = InTraits<IN>::PMAX / std::fabs((double)p->p_scale);
   kp.ovf_z = (float)std::fmin(NORM == FS_NORM_SIGNED_L1 ? pmax : pmax * pmax, 3.0e38);
   const SplitPlan sp = split_plan(p);
-  const int64_t n_qblk = (p->seqlen_q + NQT * BM - 1) / (NQT * BM);
+  const int64_t n_qblk = (p->seqlen_q + NQT * BM * CL - 1) / (NQT * BM * CL);  // per cluster
   const int64_t n_tiles = n_qblk * sp.splits * p->heads_q * p->batch;
   if (n_tiles > INT32_MAX) return fail(FS_ERR_UNSUPPORTED, "too many work tiles for one launch");
   kp.n_qblk = (int32_t)n_qblk;
@@ -1015,10 +1038,28 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
   kp.part_num = partial ? p->partial : nullptr;
   kp.part_z = partial ? p->partial + (int64_t)sp.splits * rows * D : nullptr;
-  const int grid = (int)std::min<int64_t>(n_tiles, num_sms());
+  const int grid = (int)std::min<int64_t>(n_tiles * CL, (num_sms() / CL) * CL);
   if (grid <= 0) return fail(FS_ERR_CUDA, "no SMs reported for the current device");
-  kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, tm, kp);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if constexpr (CL > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tm, kp);
+  } else {
+    kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, tm, kp);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   if (sp.splits > 1 && !p->partial_only) return combine<D>(p, sp.splits, stream);
   return FS_OK;
