@@ -98,7 +98,10 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=128 e4m3)
 #endif
 constexpr int NWT = FS_NWT;
-constexpr int CL = FS_MC ? 2 : 1;  // CTAs per cluster (sharing every K/V tile)
+#ifndef FS_CL
+#define FS_CL 2  // cluster size when FS_MC (2 or 4)
+#endif
+constexpr int CL = FS_MC ? FS_CL : 1;  // CTAs per cluster (sharing every K/V tile)
 static_assert(NWT == 4 || NWT == 8, "norm warps per Q tile");
 constexpr int NUM_THREADS = 32 * (4 + 2 * NWT + 4);
 constexpr int TMEM_COLS = 512;
@@ -1038,7 +1041,7 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
   kp.part_num = partial ? p->partial : nullptr;
   kp.part_z = partial ? p->partial + (int64_t)sp.splits * rows * D : nullptr;
-  const int grid = (int)std::min<int64_t>(n_tiles * CL, (num_sms() / CL) * CL);
+  int grid = (int)std::min<int64_t>(n_tiles * CL, (num_sms() / CL) * CL);
   if (grid <= 0) return fail(FS_ERR_CUDA, "no SMs reported for the current device");
   cudaError_t e;
   if constexpr (CL > 1) {
@@ -1054,6 +1057,19 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // persistent grid: never more clusters than can be co-resident (a GPC with an odd SM count
+    // holds one pair fewer), or the surplus clusters would run as a second wave
+    static int max_clusters[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64) {
+      if (max_clusters[dev] == 0) {
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) max_clusters[dev] = n;
+      }
+      if (max_clusters[dev] > 0) grid = std::min(grid, max_clusters[dev] * CL);
+    }
+    cfg.gridDim = dim3(grid);
     e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tm, kp);
   } else {
     kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, tm, kp);
