@@ -273,10 +273,11 @@ def multiplicity_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, m,
 
         multi_head_attention_array(q, apply_multiplicity_array(k, m), v, spec, h, h_kv, ...)
 
-    (grn.py:150 + 171-173; attention.py:381-388, 318-361) without materialising K' = m K:
-    the kernel scales each score, s_ij -> m_j s_ij, in fp32.  Same validation and errors
-    as the two reference calls (ShapeMismatchError for a length mismatch, ValueError for
-    negative or non-finite m).
+    (grn.py:150 + 171-173; attention.py:381-388, 318-361) in one call.  Same validation and
+    errors as the two reference calls (ShapeMismatchError for a length mismatch, ValueError
+    for negative or non-finite m).  K' = m K is formed in float64 before the single rounding
+    to the compute dtype; the torch entry ``flashsign.fwd(key_scale=m)`` instead scales each
+    score inside the kernel (no K' at all, but slower on the d=64 GRN shape).
     """
     mv = np.asarray(m, dtype=np.float64)
     if mv.ndim != 1 or k.ndim < 1 or mv.shape[0] != k.shape[0]:
@@ -303,7 +304,12 @@ def multiplicity_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, m,
         if q.dtype != np.float32:
             raise ConfigError("f16 emulation requires float32 inputs")
         compute = "fp16"
-    return _gpu_streamed(q, k, v, eff_scale, spec.denom_epsilon, compute, meter, norm, mv)
+    # K' = m K in float64 before the one rounding to the compute dtype (the reference's order,
+    # attention.py:381-388); measured faster end to end than the in-kernel per-score scale
+    # (flashsign.fwd(key_scale=...)), which costs the latency-bound norm step more than the
+    # elementwise pass costs
+    kp = np.asarray(k, dtype=np.float64) * mv.reshape((-1,) + (1,) * (k.ndim - 1))
+    return _gpu_streamed(q, kp.astype(k.dtype, copy=False), v, eff_scale, spec.denom_epsilon, compute, meter, norm)
 
 
 def naive_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: NormalizerSpec, scale: float,
