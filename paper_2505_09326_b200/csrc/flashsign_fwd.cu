@@ -22,6 +22,13 @@
 //   warps 20-23  epilogue WG    O_t -> registers (frees TMEM for the next work tile),
 //                               O = acc * c / b(z + eps) -> global, or fp32 partials (split K/V)
 //
+// CTAs run in clusters of two on adjacent query blocks of the same (batch, head, K/V range).
+// d=128 16-bit (Cfg::P2): the pair is one tcgen05 CTA pair -- the rank-0 CTA issues M=256
+// cta_group::2 MMAs over both CTAs' Q tiles; each CTA's ring holds half of every K/V tile (K: its
+// 64 keys; V: its 64 columns), its TMA loads complete on the leader's barriers, and the peer's
+// norm / epilogue warps arrive on the leader's p_full / o_empty remotely.  Otherwise each CTA
+// issues its own MMAs and every K/V tile is TMA-multicast into both CTAs (each loads half).
+//
 // Normalisers (compile-time NORM): spherical (a2 = s^2, b = sqrt) and signed L1 (a2 = |s|,
 // b = id), normalizers.py:94-117.  KS: per-key multiplicities m_j scale the scores in fp32.
 //
@@ -97,6 +104,12 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_STAGES16
 #define FS_STAGES16 8  // K/V ring depth for 16 KB slots (d=128 e4m3)
 #endif
+#ifndef FS_2SM
+// CTA pairs run M=256 tcgen05.mma.cta_group::2, each CTA holding half of every K/V tile:
+// 0 off, 1 for d=128 16-bit inputs (C3 +2.4 %: half the shared-memory fill and operand reads per
+// SM, one issuer per pair), 2 for every configuration (d=64 / e4m3: -1 to -2 % per GHz, measured)
+#define FS_2SM 1
+#endif
 constexpr int NWT = FS_NWT;
 #ifndef FS_CL
 #define FS_CL 2  // cluster size when FS_MC (2 or 4)
@@ -168,15 +181,31 @@ struct Cfg {
   static constexpr int BOXW = 128 / EB;        // elements per TMA box row
   static constexpr int BN = bn_for(IN, D);
   static constexpr int Q_TILE_BYTES = BM * ROW_BYTES;
-  static constexpr int SLOT_BYTES = BN * ROW_BYTES;
+  // CTA-pair MMA (cta_group::2, M = 256): the pair leader issues every MMA for both CTAs; a CTA's
+  // ring slot holds half of a K/V tile -- K: its BN/2 keys, all columns; V: all BN keys, its half
+  // of the columns (the MMA's B operand is split along N between the pair).  The multiplicity
+  // variant (KS) keeps one MMA per CTA with multicast K/V.
+  static constexpr bool P2 = FS_2SM && CL == 2 && !KS && (FS_2SM == 2 || (!TR::F8 && D == 128));
+  static constexpr int KROWS = P2 ? BN / 2 : BN;                   // K rows in a CTA's slot
+  static constexpr int VROW_BYTES = P2 ? ROW_BYTES / 2 : ROW_BYTES;  // bytes per key in a CTA's V slot
+  static constexpr int V_SW = (VROW_BYTES % 128 == 0) ? 128 : 64;  // V slot swizzle span (B)
+  static_assert(!P2 || VROW_BYTES == 128 || VROW_BYTES == 64, "pair V slot: 64 or 128 B per key");
+  static constexpr int SLOT_BYTES = P2 ? BN * ROW_BYTES / 2 : BN * ROW_BYTES;
+  // O accumulators double-buffered in TMEM when they still fit: the epilogue never gates the MMAs.
+  static constexpr int NOB_ = (2 * BN + 2 * NQT * D <= TMEM_COLS) ? 2 : 1;
   // 32 KB slots (d=128, 16-bit): one Q buffer per tile, 4 ring slots.  16 KB slots (d=128 e4m3):
   // Q double-buffered (the next work tile's Q lands during this one), 8 ring slots.  24 KB slots
-  // (d=64 16-bit, 192 keys): double-buffered Q, 6 ring slots.
-  static constexpr int NQB = (SLOT_BYTES >= 32768) ? 1 : 2;
+  // (d=64 16-bit, 192 keys): double-buffered Q, 6 ring slots.  CTA pairs: half-size slots, as
+  // many as fit (even, <= 16).
+  static constexpr int NQB = P2 ? (Q_TILE_BYTES >= 32768 ? 1 : 2) : (SLOT_BYTES >= 32768) ? 1 : 2;
+  static constexpr int P2_STAGES =
+      std::min(16, ((232448 - 1024 - 512 - NQT * NOB_ * 2 * BM * 4 - NQT * NQB * Q_TILE_BYTES) / SLOT_BYTES) & ~1);
   // (32 KB slots: a fifth slot fits when no per-key multiplicity ring is needed and the dynamic
   //  shared-memory base is 1024-aligned -- checked on the device, see SLACK)
-  static constexpr int STAGES = (SLOT_BYTES >= 32768) ? (KS ? 4 : FS_STAGES32)
+  static constexpr int STAGES = P2 ? P2_STAGES
+                                : (SLOT_BYTES >= 32768) ? (KS ? 4 : FS_STAGES32)
                                 : (SLOT_BYTES > 16384 ? 6 : FS_STAGES16);
+  static_assert(STAGES <= 16, "ring barriers");
   // K_j and V_j share one ring barrier when the ring is deep (8 slots): one wait per K/V tile on
   // the MMA issuer.  With 4 slots the pair would halve the prefetch distance (measured -10 % at C3).
   static constexpr bool KV1 = FS_KV1 && STAGES >= FS_KV1_MIN;
@@ -187,8 +216,8 @@ struct Cfg {
   // S buffers in TMEM: one per Q tile (P aliases its S).  (A third rotating buffer at d=64, for
   // a four-MMA norm window, measured slower with a generic issuer; see profiles/r1/SUMMARY.md.)
   static constexpr int NSB = 2;
-  // O accumulators double-buffered in TMEM when they still fit: the epilogue never gates the MMAs.
-  static constexpr int NOB = (NSB * BN + 2 * NQT * D <= TMEM_COLS) ? 2 : 1;
+  static constexpr int NOB = NOB_;
+  static_assert(NSB == 2, "NOB_ assumes two S buffers");
   // per-key multiplicities m_j of each V slot's keys (fused K' = m K, grn.py:150)
   static constexpr int MS_OFF = ZBUF_OFF + NQT * NOB * 2 * BM * 4;
   static constexpr int MS_SLOT_BYTES = BN * 4;
@@ -197,19 +226,20 @@ struct Cfg {
   static constexpr int SLACK = (LAYOUT_BYTES + 1024 <= 232448) ? 1024 : 0;
   static constexpr int SMEM_BYTES = LAYOUT_BYTES + SLACK;
   static constexpr int QK_STEPS = ROW_BYTES / 32;                          // 32 B of K-dim per MMA
+  static constexpr int MMA_M = P2 ? 2 * BM : BM;
   static constexpr int PV_STEPS = BN / TR::KSTEP;
   static constexpr uint32_t COL_S0 = 0;
   static constexpr uint32_t COL_O0 = NSB * BN;
   static_assert(NSB * BN + NOB * NQT * D <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(PV_STEPS % 2 == 0, "P is produced in two column halves");
-  static constexpr uint32_t IDESC_QK = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, BM, BN);
-  static constexpr uint32_t IDESC_PV = ptx::idesc_make(TR::FMT, TR::FMT, 0, 1, BM, D);
+  static constexpr uint32_t IDESC_QK = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, MMA_M, BN);
+  static constexpr uint32_t IDESC_PV = ptx::idesc_make(TR::FMT, TR::FMT, 0, 1, MMA_M, D);
 };
 
 struct Bars {
   uint64_t q_full[NQT][2], q_empty[NQT][2];
-  uint64_t kv_full[8], kv_empty[8];
+  uint64_t kv_full[16], kv_empty[16];
   uint64_t s_full[2];       // per S buffer (= Q tile)
   uint64_t p_full[2];       // per S buffer: all 8 norm warps of the tile have written P
   uint64_t o_full[NQT][2], o_empty[NQT][2];
@@ -326,7 +356,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&bars->s_full[b], 1);
-      ptx::mbar_init(&bars->p_full[b], 8);  // 2 column halves x 4 lane quarters
+      ptx::mbar_init(&bars->p_full[b], C::P2 ? 16 : 8);  // 2 column halves x 4 lane quarters (x 2 CTAs)
     }
 #pragma unroll
     for (int t = 0; t < NQT; ++t) {
@@ -335,14 +365,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_init(&bars->q_full[t][b], 1);
         ptx::mbar_init(&bars->q_empty[t][b], 1);
         ptx::mbar_init(&bars->o_full[t][b], 1);
-        ptx::mbar_init(&bars->o_empty[t][b], 4);
+        ptx::mbar_init(&bars->o_empty[t][b], C::P2 ? 8 : 4);
         ptx::mbar_init(&bars->z_full[t][b], NWT);
         ptx::mbar_init(&bars->z_empty[t][b], 4);
       }
     }
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&bars->kv_full[s], 1);
-      ptx::mbar_init(&bars->kv_empty[s], CL);  // both CTAs of a cluster consume every slot
+      ptx::mbar_init(&bars->kv_empty[s], C::P2 ? 1 : CL);  // both CTAs' MMAs (multicast) / the pair MMA
     }
     ptx::fence_barrier_init();
     ptx::fence_proxy_async();
@@ -353,7 +383,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tma_prefetch_desc(&tm_v);
     if (KS) ptx::tma_prefetch_desc(&tm_m);
   }
-  if (warp == 2) ptx::tmem_alloc(&bars->tmem_base, TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (C::P2)
+      ptx::tmem_alloc2(&bars->tmem_base, TMEM_COLS);
+    else
+      ptx::tmem_alloc(&bars->tmem_base, TMEM_COLS);
+  }
   ptx::tc_fence_before();
   if (CL > 1)
     ptx::cluster_sync();  // the peer's barriers exist before anything is multicast into them
@@ -361,6 +396,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  // CTA pair: the leader (rank 0) owns the barriers the MMAs wait on (q_full, kv_full, p_full,
+  // o_empty); the peer's TMA loads complete on them and its norm / epilogue warps arrive remotely
+  auto lead = [&](uint64_t* bar) { return ptx::mapa(ptx::smem_u32(bar), 0u); };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -376,12 +414,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int t = 0; t < NQT; ++t) {
           ptx::mbar_wait(&bars->q_empty[t][qb], (q_use & 1u) ^ 1u);
-          ptx::mbar_arrive_expect_tx(&bars->q_full[t][qb], C::Q_TILE_BYTES);
+          if (!C::P2 || rank == 0) ptx::mbar_arrive_expect_tx(&bars->q_full[t][qb], (C::P2 ? 2 : 1) * C::Q_TILE_BYTES);
 #pragma unroll
-          for (int db = 0; db < C::NDB; ++db)
-            ptx::tma_load_4d(smem + (t * C::NQB + qb) * C::Q_TILE_BYTES + db * (BM * 128), &tm_q,
-                             &bars->q_full[t][qb], db * C::BOXW, qc.qblk * (NQT * BM) + t * BM, qc.head,
-                             qc.batch, pol_q);
+          for (int db = 0; db < C::NDB; ++db) {
+            uint8_t* dst = smem + (t * C::NQB + qb) * C::Q_TILE_BYTES + db * (BM * 128);
+            const int row0 = qc.qblk * (NQT * BM) + t * BM;
+            if constexpr (C::P2)
+              ptx::tma_load_4d_2sm(dst, &tm_q, lead(&bars->q_full[t][qb]), db * C::BOXW, row0, qc.head, qc.batch,
+                                   pol_q);
+            else
+              ptx::tma_load_4d(dst, &tm_q, &bars->q_full[t][qb], db * C::BOXW, row0, qc.head, qc.batch, pol_q);
+          }
         }
       };
       load_q(tile0, 0);
@@ -408,7 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t round = kv_i / C::STAGES;
           const bool with_m = KS && (i & 1);  // V slots also carry the tile's key multiplicities
           uint64_t* full = &bars->kv_full[C::kv_bar(slot)];
-          if (FS_TMA_ONCE && kv_i >= C::STAGES) {  // experiment: no K/V traffic after the first ring
+          if (FS_TMA_ONCE && !C::P2 && kv_i >= C::STAGES) {  // experiment: no K/V traffic after the first ring
             if (!C::KV1 || !(i & 1)) {
               ptx::mbar_wait(&bars->kv_empty[C::kv_bar(slot)], (round & 1u) ^ 1u);
               ptx::mbar_arrive(full);
@@ -418,14 +461,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (!C::KV1 || !(i & 1)) {
             ptx::mbar_wait(&bars->kv_empty[C::kv_bar(slot)], (round & 1u) ^ 1u);
-            // with KV1 the K load announces both tiles' bytes (V follows right after)
-            ptx::mbar_arrive_expect_tx(full, (C::KV1 ? 2 : 1) * C::SLOT_BYTES + (KS ? C::MS_SLOT_BYTES : 0) *
-                                                                                   (C::KV1 ? 1 : (i & 1)));
+            // with KV1 the K load announces both tiles' bytes (V follows right after); a pair's
+            // leader announces both CTAs' halves
+            if (!C::P2 || rank == 0)
+              ptx::mbar_arrive_expect_tx(full, (C::P2 ? 2 : 1) * (C::KV1 ? 2 : 1) * C::SLOT_BYTES +
+                                                   (KS ? C::MS_SLOT_BYTES : 0) * (C::KV1 ? 1 : (i & 1)));
           }
           const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
           const int key0 = (tc.kb0 + (i >> 1)) * BN;
           if (with_m)
             ptx::tma_load_2d(smem + C::MS_OFF + slot * C::MS_SLOT_BYTES, &tm_m, full, key0, tc.batch, pol_kv);
+          if constexpr (C::P2) {
+            uint8_t* dst = smem + C::RING_OFF + slot * C::SLOT_BYTES;
+            const uint32_t fl = lead(full);
+            if (!(i & 1)) {  // K: this CTA's BN/2 keys, every column block
+#pragma unroll
+              for (int db = 0; db < C::NDB; ++db)
+                ptx::tma_load_4d_2sm(dst + db * (C::KROWS * 128), &tm_k, fl, db * C::BOXW, key0 + rank * C::KROWS,
+                                     head_kv, tc.batch, pol_kv);
+            } else {  // V: every key of the tile, this CTA's half of the columns
+              ptx::tma_load_4d_2sm(dst, &tm_v, fl, rank * (C::VROW_BYTES / C::EB), key0, head_kv, tc.batch, pol_kv);
+            }
+          } else
 #pragma unroll
           for (int db = 0; db < C::NDB; ++db) {
             uint8_t* dst = smem + C::RING_OFF + slot * C::SLOT_BYTES + db * (BN * 128);
@@ -444,20 +501,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs the (warp-uniform) control flow and waits; one elected
     // lane issues.  Descriptors are built once; per-step offsets are constants.
-    if (n_kv_tiles > 0) {
+    // (CTA pair: the leader issues the M=256 MMAs of both CTAs; the peer's warp 1 idles)
+    if (n_kv_tiles > 0 && (!C::P2 || rank == 0)) {
       const bool leader = ptx::elect_one();
       // every lane runs the issue code; the elected lane's predicate makes it the only issuer
       const uint32_t lp = leader ? 1u : 0u;
+      constexpr uint16_t ALL = static_cast<uint16_t>((1u << CL) - 1u);
       // a ring slot is free once every CTA of the cluster has consumed it
       auto kv_release = [&](uint64_t* bar) {
-        if constexpr (CL > 1)
-          ptx::tc_commit_mc_p(bar, static_cast<uint16_t>((1u << CL) - 1u), lp);
+        if constexpr (C::P2)
+          ptx::tc2_commit_mc_p(bar, ALL, lp);
+        else if constexpr (CL > 1)
+          ptx::tc_commit_mc_p(bar, ALL, lp);
+        else
+          ptx::tc_commit_p(bar, lp);
+      };
+      // MMA-completion signals every CTA waits on (S ready, Q buffer free, O ready)
+      auto signal = [&](uint64_t* bar) {
+        if constexpr (C::P2)
+          ptx::tc2_commit_mc_p(bar, ALL, lp);
         else
           ptx::tc_commit_p(bar, lp);
       };
       const uint64_t q_desc = ptx::sdesc_sw128(smem_s, 16, 1024);
       const uint64_t k_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, 16, 1024);
-      const uint64_t v_desc = ptx::sdesc_sw128(smem_s + C::RING_OFF, BN * 128, 1024);
+      const uint64_t v_desc = C::V_SW == 128 ? ptx::sdesc_sw128(smem_s + C::RING_OFF, BN * 128, 1024)
+                                             : ptx::sdesc_sw64(smem_s + C::RING_OFF, BN * 64, 512);
 #if FS_PROF
       long long pr_pw = 0, pr_pn = 0, pr_kw = 0, pr_kn = 0;
       const long long pr_t0 = clock64();
@@ -479,8 +548,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int ks = 0; ks < C::QK_STEPS; ++ks) {
             const uint32_t off_a = ((ks * 32 / 128) * (BM * 128) + (ks * 32) % 128) >> 4;
-            const uint32_t off_b = ((ks * 32 / 128) * (BN * 128) + (ks * 32) % 128) >> 4;
-            if constexpr (TR::F8)
+            const uint32_t off_b = ((ks * 32 / 128) * (C::KROWS * 128) + (ks * 32) % 128) >> 4;
+            if constexpr (C::P2 && TR::F8)
+              ptx::mma2_f8_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
+            else if constexpr (C::P2)
+              ptx::mma2_f16_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
+            else if constexpr (TR::F8)
               ptx::mma_f8_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
             else
               ptx::mma_f16_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
@@ -489,14 +562,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // O_t += P_t V_j once all of P_t is in TMEM (one hand-off per tile: every extra
         // barrier round trip on the issuing warp costs more than it overlaps, measured)
         auto pv = [&](int t, uint32_t slot, int j) {
-          if (j == 0) ptx::mbar_wait(&bars->o_empty[t][ob], (o_use & 1u) ^ 1u);
+          if (j == 0) {
+            if constexpr (C::P2)
+              ptx::mbar_wait_cluster(&bars->o_empty[t][ob], (o_use & 1u) ^ 1u);
+            else
+              ptx::mbar_wait(&bars->o_empty[t][ob], (o_use & 1u) ^ 1u);
+          }
           const uint64_t b0 = v_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
           const uint32_t a_tmem = tmem + C::COL_S0 + t * BN;
           const uint32_t d_tmem = tmem + C::COL_O0 + (ob * NQT + t) * D;
 #if FS_PROF
           const long long tw0 = clock64();
 #endif
-          ptx::mbar_wait(&bars->p_full[t], p_use[t] & 1u);
+          if constexpr (C::P2)
+            ptx::mbar_wait_cluster(&bars->p_full[t], p_use[t] & 1u);
+          else
+            ptx::mbar_wait(&bars->p_full[t], p_use[t] & 1u);
 #if FS_PROF
           pr_pw += clock64() - tw0;
           ++pr_pn;
@@ -505,11 +586,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int ks = 0; ks < C::PV_STEPS; ++ks) {
             const int h = ks / (C::PV_STEPS / 2), k2 = ks % (C::PV_STEPS / 2);
-            const uint32_t off_b = (ks * TR::KSTEP * 128) >> 4;
+            // (V rows are 128 B per column block; a pair's V slot has VROW_BYTES per key)
+            const uint32_t off_b = (ks * TR::KSTEP * (C::P2 ? C::VROW_BYTES : 128)) >> 4;
             // P of column half h is packed into the first columns of S_t's half h
             const uint32_t at = a_tmem + h * (BN / 2) + k2 * (TR::KSTEP * C::EB / 4);
             const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
-            if constexpr (TR::F8)
+            if constexpr (C::P2 && TR::F8)
+              ptx::mma2_f8_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
+            else if constexpr (C::P2)
+              ptx::mma2_f16_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
+            else if constexpr (TR::F8)
               ptx::mma_f8_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
             else
               ptx::mma_f16_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
@@ -533,24 +619,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
           ptx::tc_fence_after();
           qk(0, k_slot);
-          ptx::tc_commit_p(&bars->s_full[0], lp);
-          if (j == L - 1) ptx::tc_commit_p(&bars->q_empty[0][qb], lp);
+          signal(&bars->s_full[0]);
+          if (j == L - 1) signal(&bars->q_empty[0][qb]);
           if (j > 0) {
             pv(1, prev_v_slot, j - 1);
             kv_release(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
           }
           qk(1, k_slot);
-          ptx::tc_commit_p(&bars->s_full[1], lp);
+          signal(&bars->s_full[1]);
           if (!C::KV1) kv_release(&bars->kv_empty[k_slot]);  // KV1: freed with V after PV1
-          if (j == L - 1) ptx::tc_commit_p(&bars->q_empty[1][qb], lp);
+          if (j == L - 1) signal(&bars->q_empty[1][qb]);
           if (!C::KV1) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
           pv(0, v_slot, j);
-          if (j == L - 1) ptx::tc_commit_p(&bars->o_full[0][ob], lp);
+          if (j == L - 1) signal(&bars->o_full[0][ob]);
           prev_v_slot = v_slot;
         }
         pv(1, prev_v_slot, L - 1);
         kv_release(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
-        ptx::tc_commit_p(&bars->o_full[1][ob], lp);
+        signal(&bars->o_full[1][ob]);
         kv_i += 2 * L;
       }
       }
@@ -689,7 +775,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&bars->p_full[sb]);
+        if (lane == 0) {
+          if (C::P2 && rank != 0)
+            ptx::mbar_arrive_cluster(lead(&bars->p_full[sb]));  // the pair leader issues PV
+          else
+            ptx::mbar_arrive(&bars->p_full[sb]);
+        }
 #if FS_PROF
         pr_nc += clock64() - tn1;
         ++pr_nn;
@@ -768,7 +859,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (c == D / 32 - 1) {  // all of O_t is in registers: release the accumulator
               ptx::tc_fence_before();
               __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(&bars->o_empty[t][ob]);
+              if (lane == 0) {
+                if (C::P2 && rank != 0)
+                  ptx::mbar_arrive_cluster(lead(&bars->o_empty[t][ob]));
+                else
+                  ptx::mbar_arrive(&bars->o_empty[t][ob]);
+              }
             }
           } else {
 #pragma unroll
@@ -791,10 +887,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, TMEM_COLS);
+  if constexpr (C::P2) {
+    ptx::cluster_sync();  // both CTAs are done with the pair's TMEM and with each other's barriers
+    if (warp == 2) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc2(tmem, TMEM_COLS);
+    }
+  } else {
+    __syncthreads();
+    if (warp == 2) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc(tmem, TMEM_COLS);
+    }
   }
   if (CL > 1) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
 }
@@ -822,7 +926,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 static bool encode_bshd(CUtensorMap* map, CUtensorMapDataType dt, int eb, const void* ptr, int head_dim, int seqlen,
-                        int heads, int batch, const int64_t* stride, int box_w, int box_rows, std::string* err) {
+                        int heads, int batch, const int64_t* stride, int box_w, int box_rows, std::string* err,
+                        int swizzle = 128) {
   auto enc = get_encode_fn();
   if (!enc) {
     *err = "cuTensorMapEncodeTiled unavailable (driver too old?)";
@@ -835,7 +940,8 @@ static bool encode_bshd(CUtensorMap* map, CUtensorMapDataType dt, int eb, const 
   cuuint32_t box[4] = {(cuuint32_t)box_w, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, dt, 4, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r);
     return false;
@@ -1003,8 +1109,9 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
                    &err) ||
       !encode_bshd(&tk, dt, C::EB, p->k, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->k_stride, C::BOXW,
                    C::BN / CL, &err) ||
-      !encode_bshd(&tv, dt, C::EB, p->v, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->v_stride, C::BOXW,
-                   C::BN / CL, &err))
+      // V: multicast halves of the key rows, or (CTA pair) this CTA's half of the columns, all keys
+      !encode_bshd(&tv, dt, C::EB, p->v, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->v_stride,
+                   C::P2 ? C::VROW_BYTES / C::EB : C::BOXW, C::P2 ? C::BN : C::BN / CL, &err, C::V_SW))
     return fail(FS_ERR_UNSUPPORTED, err);
   CUtensorMap tm = tq;  // unused unless KS
   if (KS && !encode_key_scale(&tm, p, &err)) return fail(FS_ERR_UNSUPPORTED, err);

@@ -63,6 +63,13 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// shared::cluster address of the variable at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -129,6 +136,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Arrive on an mbarrier of another CTA of the cluster (shared::cluster address from mapa).
+// Default (.release.cta) semantics, as for the TMEM hand-offs between the CTAs of a pair:
+// the writer's tcgen05.wait::st + tcgen05.fence::before_thread_sync and the MMA thread's
+// tcgen05.fence::after_thread_sync order the TMEM accesses.  (.release.cluster compiles to a
+// MEMBAR.ALL.GPU and doubled the norm step, measured.)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// Wait on a local barrier whose arrivals come from other CTAs of the cluster (acquire.cluster).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  auto probe = [&]() {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    return ok != 0;
+  };
+  if (probe()) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  while (!probe()) {
+    if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+  }
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -165,6 +203,18 @@ __device__ __forceinline__ void tma_load_4d_mc(void* smem_dst, const void* tmap,
       : "memory");
 }
 
+// CTA-pair load (cta_group::2): the box lands in this CTA's shared memory and completes its
+// bytes on the mbarrier at `bar_cluster` (a shared::cluster address, e.g. the pair leader's).
+__device__ __forceinline__ void tma_load_4d_2sm(void* smem_dst, const void* tmap, uint32_t bar_cluster, int c0,
+                                                int c1, int c2, int c3, uint64_t cache_policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "l"(cache_policy)
+      : "memory");
+}
+
 // Pull a tile into L2 ahead of its real load (no shared-memory destination, no barrier).
 __device__ __forceinline__ void tma_prefetch_l2_4d(const void* tmap, int c0, int c1, int c2, int c3) {
   asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
@@ -191,6 +241,18 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
                "r"(ncols)
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+// CTA-pair allocation: one warp (same warp index) of each CTA of the pair executes it; the
+// same columns are allocated in both CTAs' TMEM.
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
@@ -275,6 +337,41 @@ __device__ __forceinline__ void tc_commit_mc_p(uint64_t* bar, uint16_t mask, uin
       "h"(mask), "r"(pred)
       : "memory");
 }
+
+// CTA-pair forms (cta_group::2, issued by the pair leader only): M = 256 over the two CTAs'
+// TMEM lanes; A from each CTA's shared memory / TMEM at the same address, B split along N
+// between the two CTAs' shared memory; commits arrive on the barrier at this offset in every
+// CTA of `mask`.
+__device__ __forceinline__ void tc2_commit_mc_p(uint64_t* bar, uint16_t mask, uint32_t pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ne.b32 q, %2, 0;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask), "r"(pred)
+      : "memory");
+}
+
+#define FS_MMA2_P(NAME, KIND, AOP, ATYPE, ACON)                                                              \
+  __device__ __forceinline__ void NAME(uint32_t d_tmem, ATYPE a, uint64_t b_desc, uint32_t idesc,           \
+                                       uint32_t accumulate, uint32_t pred) {                                \
+    asm volatile(                                                                                           \
+        "{\n\t.reg .pred p, q;\n\t"                                                                     \
+        "setp.ne.b32 p, %4, 0;\n\t"                                                                       \
+        "setp.ne.b32 q, %5, 0;\n\t"                                                                       \
+        "@q tcgen05.mma.cta_group::2.kind::" KIND " [%0], " AOP ", %2, %3, p;\n\t}" ::"r"(d_tmem),          \
+        ACON(a), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(pred)                                       \
+        : "memory");                                                                                        \
+  }
+#define FS_CON_L(a) "l"(a)
+#define FS_CON_R(a) "r"(a)
+FS_MMA2_P(mma2_f16_ss_p, "f16", "%1", uint64_t, FS_CON_L)
+FS_MMA2_P(mma2_f8_ss_p, "f8f6f4", "%1", uint64_t, FS_CON_L)
+FS_MMA2_P(mma2_f16_ts_p, "f16", "[%1]", uint32_t, FS_CON_R)
+FS_MMA2_P(mma2_f8_ts_p, "f8f6f4", "[%1]", uint32_t, FS_CON_R)
+#undef FS_MMA2_P
+#undef FS_CON_L
+#undef FS_CON_R
 
 #define FS_MMA_P(NAME, KIND, AOP, ATYPE)                                                                     \
   __device__ __forceinline__ void NAME(uint32_t d_tmem, ATYPE a, uint64_t b_desc, uint32_t idesc,           \
@@ -381,6 +478,18 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr, uint32_t lbo
   d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
   d |= 1ull << 46;  // descriptor version (sm100)
   d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// SWIZZLE_64B (MN-major operand whose MN extent is 64 B per K-row: 8 K-rows per 512 B atom,
+// SBO = distance between 8-row groups, LBO = distance between 64 B MN column blocks).
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;  // descriptor version (sm100)
+  d |= 4ull << 61;  // SWIZZLE_64B
   return d;
 }
 
