@@ -110,6 +110,12 @@ constexpr int NQT = 2;   // Q tiles per work tile
 // SM, one issuer per pair), 2 for every configuration (d=64 / e4m3: -1 to -2 % per GHz, measured)
 #define FS_2SM 1
 #endif
+#ifndef FS_P2_NQB2
+#define FS_P2_NQB2 0  // CTA pairs at d=128: double-buffer Q (fewer ring slots)
+#endif
+#ifndef FS_P2_STAGES
+#define FS_P2_STAGES 0  // CTA-pair ring depth override (0: as many half-tile slots as fit)
+#endif
 constexpr int NWT = FS_NWT;
 #ifndef FS_CL
 #define FS_CL 2  // cluster size when FS_MC (2 or 4)
@@ -197,12 +203,12 @@ struct Cfg {
   // Q double-buffered (the next work tile's Q lands during this one), 8 ring slots.  24 KB slots
   // (d=64 16-bit, 192 keys): double-buffered Q, 6 ring slots.  CTA pairs: half-size slots, as
   // many as fit (even, <= 16).
-  static constexpr int NQB = P2 ? (Q_TILE_BYTES >= 32768 ? 1 : 2) : (SLOT_BYTES >= 32768) ? 1 : 2;
+  static constexpr int NQB = P2 ? (Q_TILE_BYTES >= 32768 && !FS_P2_NQB2 ? 1 : 2) : (SLOT_BYTES >= 32768) ? 1 : 2;
   static constexpr int P2_STAGES =
       std::min(16, ((232448 - 1024 - 512 - NQT * NOB_ * 2 * BM * 4 - NQT * NQB * Q_TILE_BYTES) / SLOT_BYTES) & ~1);
   // (32 KB slots: a fifth slot fits when no per-key multiplicity ring is needed and the dynamic
   //  shared-memory base is 1024-aligned -- checked on the device, see SLACK)
-  static constexpr int STAGES = P2 ? P2_STAGES
+  static constexpr int STAGES = P2 ? (FS_P2_STAGES ? std::min(FS_P2_STAGES, P2_STAGES) : P2_STAGES)
                                 : (SLOT_BYTES >= 32768) ? (KS ? 4 : FS_STAGES32)
                                 : (SLOT_BYTES > 16384 ? 6 : FS_STAGES16);
   static_assert(STAGES <= 16, "ring barriers");
