@@ -190,6 +190,26 @@ def cpu_reference_sample(cfg, rows: int, seed: int = 7):
     return dt, 4.0 * rows * N * D, threads or os.cpu_count()
 
 
+def _host_info():
+    """CPU model and BLAS backend of the host the CPU baseline ran on."""
+    info = {"cpu_model": None, "blas": None, "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = ", ".join(f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}"
+                                 for i in threadpool_info() if i.get("user_api") == "blas") or None
+    except Exception:
+        pass
+    return info
+
+
 def _all_host_threads():
     """BLAS thread pool sized to every host core (torchrun sets OMP_NUM_THREADS=1 per rank)."""
     try:
@@ -227,7 +247,7 @@ def _run_reference(args, cfg):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "sample": sample},
         "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample,
-                         "cpu_count": os.cpu_count()},
+                         "cpu_count": os.cpu_count(), **_host_info()},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -324,12 +344,16 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # per-step events too (median / min per step); they add no work to the stream
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             step()
+            ev[i].record(stream)
         e1.record(stream)
         torch.cuda.synchronize()
+    per_step = [e0.elapsed_time(ev[0])] + [ev[i - 1].elapsed_time(ev[i]) for i in range(1, args.steps)]
     if world > 1:
         dist.barrier()
     ms_total = e0.elapsed_time(e1)
@@ -424,14 +448,17 @@ def run_ours(args, cfg):
             rows = args.cpu_rows or N
             with _all_host_threads():
                 dt, fl, threads = cpu_reference_sample(cfg, rows)
+                host = _host_info()
             cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
                    "sample": f"{rows} query rows x {N} keys x d{D}, one (b,h) slice, float32, tile 64x64 "
                              f"(oracle port of attention.py:146-200), {dt:.2f} s",
-                   "cpu_count": os.cpu_count()}
+                   "cpu_count": os.cpu_count(), **host}
         ctx = context_baselines(cfg, q, k, v, dev) if (world == 1 and args.context) else None
         line = {
             "metric": "FlashSign fwd TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "ms_per_step_median": statistics.median(per_step), "ms_per_step_min": min(per_step),
+            "higher_is_better": True,
             "scaling": "strong", "vs_baseline": value / PAPER_A100_TFLOPS,
             "vs_baseline_ref": "paper's A100 FlashSign fwd ~200 TFLOP/s (PAPER.md:199, BASELINE.md section 1)",
             "dtype": {"bf16": "bf16", "fp16": "fp16", "e4m3": "e4m3"}[cfg["dtype"]], "data": "synthetic",

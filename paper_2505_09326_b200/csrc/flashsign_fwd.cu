@@ -110,6 +110,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 // SM, one issuer per pair), 2 for every configuration (d=64 / e4m3: -1 to -2 % per GHz, measured)
 #define FS_2SM 1
 #endif
+#ifndef FS_SPLITS
+#define FS_SPLITS 0  // experiment: per-CTA MMAs issue S_t as two key halves (own S-ready / P-ready barriers)
+#endif
 #ifndef FS_P2_NQB2
 #define FS_P2_NQB2 0  // CTA pairs at d=128: double-buffer Q (fewer ring slots)
 #endif
@@ -205,7 +208,7 @@ struct Cfg {
   // many as fit (even, <= 16).
   static constexpr int NQB = P2 ? (Q_TILE_BYTES >= 32768 && !FS_P2_NQB2 ? 1 : 2) : (SLOT_BYTES >= 32768) ? 1 : 2;
   static constexpr int P2_STAGES =
-      std::min(16, ((232448 - 1024 - 512 - NQT * NOB_ * 2 * BM * 4 - NQT * NQB * Q_TILE_BYTES) / SLOT_BYTES) & ~1);
+      std::min(16, ((232448 - 1024 - 1024 - NQT * NOB_ * 2 * BM * 4 - NQT * NQB * Q_TILE_BYTES) / SLOT_BYTES) & ~1);
   // (32 KB slots: a fifth slot fits when no per-key multiplicity ring is needed and the dynamic
   //  shared-memory base is 1024-aligned -- checked on the device, see SLACK)
   static constexpr int STAGES = P2 ? (FS_P2_STAGES ? std::min(FS_P2_STAGES, P2_STAGES) : P2_STAGES)
@@ -218,7 +221,7 @@ struct Cfg {
   __device__ static uint32_t kv_bar(uint32_t slot) { return KV1 ? (slot & ~1u) : slot; }
   static constexpr int RING_OFF = NQT * NQB * Q_TILE_BYTES;
   static constexpr int BAR_OFF = RING_OFF + STAGES * SLOT_BYTES;
-  static constexpr int ZBUF_OFF = BAR_OFF + 512;
+  static constexpr int ZBUF_OFF = BAR_OFF + 1024;
   // S buffers in TMEM: one per Q tile (P aliases its S).  (A third rotating buffer at d=64, for
   // a four-MMA norm window, measured slower with a generic issuer; see profiles/r1/SUMMARY.md.)
   static constexpr int NSB = 2;
@@ -233,6 +236,11 @@ struct Cfg {
   static constexpr int SMEM_BYTES = LAYOUT_BYTES + SLACK;
   static constexpr int QK_STEPS = ROW_BYTES / 32;                          // 32 B of K-dim per MMA
   static constexpr int MMA_M = P2 ? 2 * BM : BM;
+  // Split S hand-off (per-CTA MMAs, one norm warp per column half): QK_t is issued as two
+  // key halves, each committed to its own S-ready barrier, and PV_t consumes P half by half, so
+  // each half's norm starts one half-MMA earlier and ends one half-MMA later:
+  // the norm window grows from 2 to 2.5 MMAs.
+  static constexpr bool SPLIT = FS_SPLITS && !P2 && NWT == 8;
   static constexpr int PV_STEPS = BN / TR::KSTEP;
   static constexpr uint32_t COL_S0 = 0;
   static constexpr uint32_t COL_O0 = NSB * BN;
@@ -240,19 +248,20 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(PV_STEPS % 2 == 0, "P is produced in two column halves");
   static constexpr uint32_t IDESC_QK = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, MMA_M, BN);
+  static constexpr uint32_t IDESC_QKH = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, MMA_M, BN / 2);
   static constexpr uint32_t IDESC_PV = ptx::idesc_make(TR::FMT, TR::FMT, 0, 1, MMA_M, D);
 };
 
 struct Bars {
   uint64_t q_full[NQT][2], q_empty[NQT][2];
   uint64_t kv_full[16], kv_empty[16];
-  uint64_t s_full[2];       // per S buffer (= Q tile)
-  uint64_t p_full[2];       // per S buffer: all 8 norm warps of the tile have written P
+  uint64_t s_full[2][2];    // per S buffer (= Q tile) [x key half when Cfg::SPLIT]
+  uint64_t p_full[2][2];    // per S buffer [x key half]: the tile's norm warps have written P
   uint64_t o_full[NQT][2], o_empty[NQT][2];
   uint64_t z_full[NQT][2], z_empty[NQT][2];
   uint32_t tmem_base;
 };
-static_assert(sizeof(Bars) <= 512, "barrier block");
+static_assert(sizeof(Bars) <= 1024, "barrier block");
 
 template <int IN>
 __device__ __forceinline__ uint32_t pack2(float lo, float hi);
@@ -361,8 +370,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 32) {
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&bars->s_full[b], 1);
-      ptx::mbar_init(&bars->p_full[b], C::P2 ? 16 : 8);  // 2 column halves x 4 lane quarters (x 2 CTAs)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        ptx::mbar_init(&bars->s_full[b][h], 1);
+        // 2 column halves x 4 lane quarters (x 2 CTAs); split: 4 lane quarters per half
+        ptx::mbar_init(&bars->p_full[b][h], C::SPLIT ? 4 : C::P2 ? 16 : 8);
+      }
     }
 #pragma unroll
     for (int t = 0; t < NQT; ++t) {
@@ -547,22 +560,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int ob = it % C::NOB;
         const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
         const int L = decode_tile(tile, p, rank).L;
-        auto qk = [&](int t, uint32_t slot) {
+        // S_t = Q_t K^T for key half h of the tile (h < 0: all BN keys)
+        auto qk = [&](int t, uint32_t slot, int h) {
+          const uint32_t hoff = h > 0 ? h * (BN / 2) : 0;  // first key (= S column) of the half
+          const uint32_t idesc = h < 0 ? C::IDESC_QK : C::IDESC_QKH;
           const uint64_t a0 = q_desc + static_cast<uint32_t>(((t * C::NQB + qb) * C::Q_TILE_BYTES) >> 4);
-          const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
-          const uint32_t d_tmem = tmem + C::COL_S0 + t * BN;
+          const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES + hoff * 128) >> 4);
+          const uint32_t d_tmem = tmem + C::COL_S0 + t * BN + hoff;
 #pragma unroll
           for (int ks = 0; ks < C::QK_STEPS; ++ks) {
             const uint32_t off_a = ((ks * 32 / 128) * (BM * 128) + (ks * 32) % 128) >> 4;
             const uint32_t off_b = ((ks * 32 / 128) * (C::KROWS * 128) + (ks * 32) % 128) >> 4;
             if constexpr (C::P2 && TR::F8)
-              ptx::mma2_f8_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
+              ptx::mma2_f8_ss_p(d_tmem, a0 + off_a, b0 + off_b, idesc, ks > 0, lp);
             else if constexpr (C::P2)
-              ptx::mma2_f16_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
+              ptx::mma2_f16_ss_p(d_tmem, a0 + off_a, b0 + off_b, idesc, ks > 0, lp);
             else if constexpr (TR::F8)
-              ptx::mma_f8_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
+              ptx::mma_f8_ss_p(d_tmem, a0 + off_a, b0 + off_b, idesc, ks > 0, lp);
             else
-              ptx::mma_f16_ss_p(d_tmem, a0 + off_a, b0 + off_b, C::IDESC_QK, ks > 0, lp);
+              ptx::mma_f16_ss_p(d_tmem, a0 + off_a, b0 + off_b, idesc, ks > 0, lp);
           }
         };
         // O_t += P_t V_j once all of P_t is in TMEM (one hand-off per tile: every extra
@@ -577,21 +593,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint64_t b0 = v_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
           const uint32_t a_tmem = tmem + C::COL_S0 + t * BN;
           const uint32_t d_tmem = tmem + C::COL_O0 + (ob * NQT + t) * D;
+          auto wait_p = [&](int h) {
 #if FS_PROF
-          const long long tw0 = clock64();
+            const long long tw0 = clock64();
 #endif
-          if constexpr (C::P2)
-            ptx::mbar_wait_cluster(&bars->p_full[t], p_use[t] & 1u);
-          else
-            ptx::mbar_wait(&bars->p_full[t], p_use[t] & 1u);
+            if constexpr (C::P2)
+              ptx::mbar_wait_cluster(&bars->p_full[t][h], p_use[t] & 1u);
+            else
+              ptx::mbar_wait(&bars->p_full[t][h], p_use[t] & 1u);
 #if FS_PROF
-          pr_pw += clock64() - tw0;
-          ++pr_pn;
+            pr_pw += clock64() - tw0;
+            ++pr_pn;
 #endif
-          ptx::tc_fence_after();
+            ptx::tc_fence_after();
+          };
+          wait_p(0);
 #pragma unroll
           for (int ks = 0; ks < C::PV_STEPS; ++ks) {
             const int h = ks / (C::PV_STEPS / 2), k2 = ks % (C::PV_STEPS / 2);
+            if (C::SPLIT && ks == C::PV_STEPS / 2) wait_p(1);  // second key half's P
             // (V rows are 128 B per column block; a pair's V slot has VROW_BYTES per key)
             const uint32_t off_b = (ks * TR::KSTEP * (C::P2 ? C::VROW_BYTES : 128)) >> 4;
             // P of column half h is packed into the first columns of S_t's half h
@@ -624,15 +644,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ++pr_kn;
 #endif
           ptx::tc_fence_after();
-          qk(0, k_slot);
-          signal(&bars->s_full[0]);
+          auto qk_signal = [&](int t) {
+            if constexpr (C::SPLIT) {
+              qk(t, k_slot, 0);
+              signal(&bars->s_full[t][0]);
+              qk(t, k_slot, 1);
+              signal(&bars->s_full[t][1]);
+            } else {
+              qk(t, k_slot, -1);
+              signal(&bars->s_full[t][0]);
+            }
+          };
+          qk_signal(0);
           if (j == L - 1) signal(&bars->q_empty[0][qb]);
           if (j > 0) {
             pv(1, prev_v_slot, j - 1);
             kv_release(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
           }
-          qk(1, k_slot);
-          signal(&bars->s_full[1]);
+          qk_signal(1);
           if (!C::KV1) kv_release(&bars->kv_empty[k_slot]);  // KV1: freed with V after PV1
           if (j == L - 1) signal(&bars->q_empty[1][qb]);
           if (!C::KV1) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
@@ -679,7 +708,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const long long tn0 = clock64();
 #endif
         const uint32_t sb = t;  // S_t's TMEM buffer; one phase per K/V tile
-        ptx::mbar_wait(&bars->s_full[sb], s_use & 1u);
+        ptx::mbar_wait(&bars->s_full[sb][C::SPLIT ? hh0 : 0], s_use & 1u);
         const uint32_t s_base = s_lane + sb * BN;
         // key multiplicities of this K/V tile ride in V_j's ring slot; that slot is released only
         // after PV_1(j), which needs this warp's P, so they stay valid while they are read here
@@ -783,9 +812,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           if (C::P2 && rank != 0)
-            ptx::mbar_arrive_cluster(lead(&bars->p_full[sb]));  // the pair leader issues PV
+            ptx::mbar_arrive_cluster(lead(&bars->p_full[sb][0]));  // the pair leader issues PV
           else
-            ptx::mbar_arrive(&bars->p_full[sb]);
+            ptx::mbar_arrive(&bars->p_full[sb][C::SPLIT ? hh : 0]);
         }
 #if FS_PROF
         pr_nc += clock64() - tn1;
