@@ -190,6 +190,28 @@ def cpu_reference_sample(cfg, rows: int, seed: int = 7):
     return dt, 4.0 * rows * N * D, threads or os.cpu_count()
 
 
+def _link_roofline(dev, h2d_bytes, d2h_bytes, step_s):
+    """Host<->device copy roofline of the e2e step: pinned 256 MiB copies each way (best of 3)
+    bound the step at max(h2d / BW_h2d, d2h / BW_d2h) when the two directions overlap."""
+    import torch
+    n = 256 << 20
+    host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    devb = torch.empty(n, dtype=torch.uint8, device=dev)
+    bw = {}
+    for name, dst, src in (("h2d", devb, host), ("d2h", host, devb)):
+        best = float("inf")
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
+        bw[name] = n / best / 1e9
+    bound = max(h2d_bytes / (bw["h2d"] * 1e9), d2h_bytes / (bw["d2h"] * 1e9))
+    return {"h2d_gbs": bw["h2d"], "d2h_gbs": bw["d2h"], "bound_ms": bound * 1e3, "frac": bound / step_s}
+
+
 def _host_info():
     """CPU model and BLAS backend of the host the CPU baseline ran on."""
     info = {"cpu_model": None, "blas": None, "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
@@ -411,13 +433,15 @@ def run_ours(args, cfg):
         elsz = q.element_size()
         h2d = (q.numel() + k.numel() + v.numel()) * elsz + (0 if mh is None else mh.numel() * 4)
         d2h = o.numel() * o.element_size()
+        link = _link_roofline(dev, h2d, d2h, dt)
         if world > 1:
             vals = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
             dist.all_reduce(vals)
             h2d, d2h = int(vals[0].item()), int(vals[1].item())
         e2e = {"value": (total_flops if world > 1 else my_flops) / dt / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
-               "steps": e2e_steps, "api": "paper_2505_09326_b200.pipeline.HostPipeline.run (pinned host bf16 in/out)"}
+               "steps": e2e_steps, "api": "paper_2505_09326_b200.pipeline.HostPipeline.run (pinned host bf16 in/out)",
+               "link": link}
 
     if rank == 0:
         peaks, peak_src = load_peaks()
