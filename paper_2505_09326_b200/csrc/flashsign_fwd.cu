@@ -1329,6 +1329,9 @@ fs_status fs_fwd(const fs_fwd_params* p, fs_stream_t stream_) {
   if ((p->head_dim * eb) % 16 != 0)
     return fail(FS_ERR_UNSUPPORTED, "head_dim * elem_bytes must be a multiple of 16 (pad the head dim)");
   if (p->heads_q > 65535 || p->batch > 65535) return fail(FS_ERR_UNSUPPORTED, "heads/batch must be <= 65535");
+  // the bad-row key carries the linear query row (b*H + h)*N + n in its upper 32 bits
+  if (static_cast<int64_t>(p->batch) * p->heads_q * p->seqlen_q > static_cast<int64_t>(UINT32_MAX))
+    return fail(FS_ERR_UNSUPPORTED, "batch * heads_q * seqlen_q must be < 2^32 (split the call)");
   auto aligned16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
   if (!aligned16(p->q) || !aligned16(p->k) || !aligned16(p->v) || !aligned16(p->o))  // NULL is aligned
     return fail(FS_ERR_UNSUPPORTED, "q/k/v/o must be 16-byte aligned");

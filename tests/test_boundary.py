@@ -93,6 +93,8 @@ def _params(**kw):
     (dict(key_scale=(1 << 20) + 4), _lib.FS_ERR_UNSUPPORTED, "key_scale must be 16-byte aligned"),
     (dict(batch=2, key_scale=1 << 20, key_scale_stride=130), _lib.FS_ERR_UNSUPPORTED, "key_scale_stride"),
     (dict(batch=2, key_scale=1 << 20, key_scale_stride=64), _lib.FS_ERR_UNSUPPORTED, "key_scale_stride"),
+    (dict(batch=65535, heads_q=65535, heads_kv=65535, seqlen_q=2), _lib.FS_ERR_UNSUPPORTED, "2^32"),
+    (dict(heads_q=70000, heads_kv=70000), _lib.FS_ERR_UNSUPPORTED, "65535"),
 ])
 def test_fs_fwd_validation(kw, status, needle):
     lib = _lib.load()
