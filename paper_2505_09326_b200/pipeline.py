@@ -34,11 +34,15 @@ class HostPipeline:
         self.s_cmp = torch.cuda.Stream(self.device)
         self.s_out = torch.cuda.Stream(self.device)
 
-    def _slices(self, nq: int, heads: int = 1) -> list[tuple[int, int]]:
+    def _slices(self, nq: int, heads: int = 1, last: bool = False) -> list[tuple[int, int]]:
         # Query slices: as many as keep >= 3 full waves of work tiles per launch (at most 4), so
         # slicing shortens the pipeline's fill/drain without leaving SMs idle in a launch's tail.
+        # The last batch chunk is cut finer (8 slices): once the final input bytes have crossed
+        # the link, only its last slice's kernel and output copy remain (the drain).
         if self.q_split is not None:
             qs = self.q_split
+        elif last:
+            qs = 8
         else:
             if self._sms is None:
                 self._sms = torch.cuda.get_device_properties(self.device).multi_processor_count
@@ -78,6 +82,7 @@ class HostPipeline:
         c = self.chunk
         nb, nq, h = q.shape[0], q.shape[1], q.shape[2]
         slices = self._slices(nq, h)
+        tail = self._slices(nq, h, last=True)
         ev_q_free = [None, None]     # compute done with Q slot / O slot producer side
         ev_o_free = [None, None]     # D2H of O slot done
         ev_kv_free = [None, None]    # last compute of a batch chunk done with its K/V slot
@@ -97,7 +102,7 @@ class HostPipeline:
                     if key_scale is not None:
                         self.dm[kvs][:n].copy_(key_scale[b0:b1], non_blocking=True)
                     ev_kv.record(self.s_in)
-                for (n0, n1) in slices:
+                for (n0, n1) in (tail if b1 >= nb and nb > c else slices):
                     s = g & 1
                     g += 1
                     nn = n1 - n0
