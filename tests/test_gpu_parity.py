@@ -441,7 +441,7 @@ def test_host_pipeline_equals_device_path():
     ref = fs().fwd(q, k, v)
     qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
     oh = torch.empty(q.shape, dtype=torch.bfloat16, pin_memory=True)
-    for chunk, qs in ((1, None), (2, None), (1, 3), (2, 2)):
+    for chunk, qs in ((1, None), (2, None), (1, 3), (2, 2), (None, None), (4, 2)):
         oh.zero_()
         HostPipeline(0, chunk=chunk, q_split=qs).run(qh, kh, vh, oh)
         assert torch.equal(oh, ref.cpu()), (chunk, qs)
