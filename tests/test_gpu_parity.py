@@ -750,3 +750,41 @@ def test_random_feature_sweep(case):
     assert err.max() <= tol * max(scale_ref, 1e-3) + 1e-6, (c, float(err.max()), float(scale_ref))
     rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
     assert rel <= {torch.float16: 4e-3, torch.bfloat16: 1.5e-2, torch.float8_e4m3fn: 8e-2}[c["dt"]], (c, rel)
+
+
+# ------------------------------------------------------------------ maximum extents
+
+@pytest.mark.parametrize("b,h,n,d,dt", [
+    (65535, 1, 3, 16, torch.bfloat16),    # largest batch the C-ABI accepts: 65535 work tiles
+    (1, 65535, 3, 16, torch.float16),     # largest head count (GQA 65535 -> 5 kv heads)
+])
+def test_maximum_batch_and_heads(b, h, n, d, dt):
+    hkv = 5 if h > 1 else 1
+    q = rand_bshd(b, n, h, d, dt, 120)
+    k = rand_bshd(b, n + 2, hkv, d, dt, 121)
+    v = rand_bshd(b, n + 2, hkv, d, dt, 122)
+    o = fs().fwd(q, k, v, out_dtype=torch.float32)
+    # every row against the exact float64 oracle: S = q K^T directly (tiny N), O = S V / |S|
+    qd, kd, vd = (t.double() for t in (q, k, v))
+    grp = h // hkv
+    kd = kd.repeat_interleave(grp, dim=2)
+    vd = vd.repeat_interleave(grp, dim=2)
+    s = torch.einsum("bnhd,bmhd->bhnm", qd, kd)
+    ref = torch.einsum("bhnm,bmhd->bnhd", s, vd) / s.pow(2).sum(-1).sqrt().permute(0, 2, 1)[..., None]
+    check_tol(o.cpu().numpy(), ref.cpu().numpy(), dt, f"b{b} h{h}")
+
+
+def test_long_sequence_million_keys():
+    # N = 2^20 queries and keys in one (b, h): 5462 K/V tiles per work tile, 4096 work tiles
+    n, d = 1 << 20, 64
+    q = rand_bshd(1, n, 1, d, torch.bfloat16, 130)
+    k = rand_bshd(1, n, 1, d, torch.bfloat16, 131)
+    v = rand_bshd(1, n, 1, d, torch.bfloat16, 132)
+    o = fs().fwd(q, k, v, kv_splits=1)
+    rows = torch.tensor([0, 1, 4095, 4096, 777777, n - 1])
+    ref = gram_spherical(q[0, rows.cuda(), 0].float().cpu().numpy(), k[0, :, 0].float().cpu().numpy(),
+                         v[0, :, 0].float().cpu().numpy(), 1.0, 0.0)
+    check_tol(o[0, rows.cuda(), 0].float().cpu().numpy(), ref, torch.bfloat16, "N=2^20")
+    # and split into 4 K/V ranges of 2^18 keys (partials + merge kernel)
+    o2 = fs().fwd(q, k, v, kv_splits=4)
+    check_tol(o2[0, rows.cuda(), 0].float().cpu().numpy(), ref, torch.bfloat16, "N=2^20 split 4")
