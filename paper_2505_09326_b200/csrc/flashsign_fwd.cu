@@ -113,6 +113,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_SPLITS
 #define FS_SPLITS 0  // experiment: per-CTA MMAs issue S_t as two key halves (own S-ready / P-ready barriers)
 #endif
+#ifndef FS_PV_TRIM
+#define FS_PV_TRIM 1  // skip the PV K-steps past the end of the sequence on a ragged last K/V tile
+#endif
 #ifndef FS_P2_NQB2
 #define FS_P2_NQB2 0  // CTA pairs at d=128: double-buffer Q (fewer ring slots)
 #endif
@@ -559,7 +562,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t q_use = static_cast<uint32_t>(it / C::NQB);
         const int ob = it % C::NOB;
         const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
-        const int L = decode_tile(tile, p, rank).L;
+        const TileCoord tcm = decode_tile(tile, p, rank);
+        const int L = tcm.L;
         // S_t = Q_t K^T for key half h of the tile (h < 0: all BN keys)
         auto qk = [&](int t, uint32_t slot, int h) {
           const uint32_t hoff = h > 0 ? h * (BN / 2) : 0;  // first key (= S column) of the half
@@ -608,23 +612,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tc_fence_after();
           };
           wait_p(0);
-#pragma unroll
-          for (int ks = 0; ks < C::PV_STEPS; ++ks) {
+          auto issue = [&](int ks, uint32_t pred) {
             const int h = ks / (C::PV_STEPS / 2), k2 = ks % (C::PV_STEPS / 2);
-            if (C::SPLIT && ks == C::PV_STEPS / 2) wait_p(1);  // second key half's P
             // (V rows are 128 B per column block; a pair's V slot has VROW_BYTES per key)
             const uint32_t off_b = (ks * TR::KSTEP * (C::P2 ? C::VROW_BYTES : 128)) >> 4;
             // P of column half h is packed into the first columns of S_t's half h
             const uint32_t at = a_tmem + h * (BN / 2) + k2 * (TR::KSTEP * C::EB / 4);
             const uint32_t acc = (j > 0 || ks > 0) ? 1u : 0u;
             if constexpr (C::P2 && TR::F8)
-              ptx::mma2_f8_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
+              ptx::mma2_f8_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, pred);
             else if constexpr (C::P2)
-              ptx::mma2_f16_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
+              ptx::mma2_f16_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, pred);
             else if constexpr (TR::F8)
-              ptx::mma_f8_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
+              ptx::mma_f8_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, pred);
             else
-              ptx::mma_f16_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, lp);
+              ptx::mma_f16_ts_p(d_tmem, at, b0 + off_b, C::IDESC_PV, acc, pred);
+          };
+          // keys of this K/V tile inside the sequence: on a ragged last tile the K-steps past them
+          // would multiply P = 0 (zero-filled K rows) with zero-filled V rows -- not issued
+          const int keys_left = p.seqlen_kv - (tcm.kb0 + j) * BN;
+          if (FS_PV_TRIM && keys_left < BN) {
+            const int n_steps = (keys_left + TR::KSTEP - 1) / TR::KSTEP;
+#pragma unroll 1
+            for (int ks = 0; ks < n_steps; ++ks) {
+              if (C::SPLIT && ks == C::PV_STEPS / 2) wait_p(1);
+              issue(ks, lp);
+            }
+            if (C::SPLIT && n_steps <= C::PV_STEPS / 2) wait_p(1);  // keep the phase accounting
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < C::PV_STEPS; ++ks) {
+              if (C::SPLIT && ks == C::PV_STEPS / 2) wait_p(1);  // second key half's P
+              issue(ks, lp);
+            }
           }
           ++p_use[t];
         };
