@@ -159,7 +159,8 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
         for t in (out, bad_key, partial, key_scale):
             if t is not None:
                 t.record_stream(stream)
-    st = lib.fs_fwd(ctypes.byref(prm), ctypes.c_void_p(stream.cuda_stream))
+    with torch.cuda.device(q.device):  # the C-ABI launches on the current device
+        st = lib.fs_fwd(ctypes.byref(prm), ctypes.c_void_p(stream.cuda_stream))
     if st != _lib.FS_OK:
         raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
     if partial_only:
@@ -218,8 +219,19 @@ def combine(partial: torch.Tensor, n_parts: int, like_q: torch.Tensor, *, out: t
     if out_dtype is None:
         out_dtype = out.dtype if out is not None else (like_q.dtype if like_q.dtype in (torch.bfloat16, torch.float16)
                                                        else torch.bfloat16)
+    if out_dtype not in _OUT_CODES or like_q.dtype not in _IN_CODES:
+        raise ShapeMismatchError(f"flashsign: unsupported dtypes {like_q.dtype} -> {out_dtype}")
     if out is None:
         out = torch.empty((b, nq, h, d), dtype=out_dtype, device=like_q.device)
+    elif (tuple(out.shape) != (b, nq, h, d) or out.dtype != out_dtype or out.stride(-1) != 1
+          or out.device != like_q.device):
+        raise ShapeMismatchError(f"flashsign: bad out tensor {tuple(out.shape)} {out.dtype}")
+    dk = 128 if (like_q.dtype not in (torch.bfloat16, torch.float16) or d > 64) else 64
+    need = int(n_parts) * b * h * nq * (dk + 1)
+    if (n_parts < 1 or partial.dtype != torch.float32 or not partial.is_contiguous()
+            or partial.numel() < need or partial.device != like_q.device):
+        raise ShapeMismatchError(f"flashsign: combine needs a contiguous float32 partial of >= {need} elements "
+                                 f"({n_parts} parts) on {like_q.device}")
     if bad_key is None:
         bad_key = torch.empty(1, dtype=torch.int64, device=like_q.device)
     prm = _lib.FsFwdParams()
@@ -232,7 +244,8 @@ def combine(partial: torch.Tensor, n_parts: int, like_q: torch.Tensor, *, out: t
     if stream is None:
         with torch.cuda.device(like_q.device):
             stream = torch.cuda.current_stream()
-    st = _lib.load().fs_combine(ctypes.byref(prm), int(n_parts), ctypes.c_void_p(stream.cuda_stream))
+    with torch.cuda.device(like_q.device):
+        st = _lib.load().fs_combine(ctypes.byref(prm), int(n_parts), ctypes.c_void_p(stream.cuda_stream))
     if st != _lib.FS_OK:
         raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
     if check:

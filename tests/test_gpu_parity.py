@@ -660,6 +660,21 @@ def test_context_parallel_emulated_on_one_gpu(world):
     assert float((o2 - full).abs().max()) <= 2e-5 * max(1.0, float(full.abs().max()))
 
 
+def test_combine_validates_workspace_and_output():
+    from paper_2505_09326_b200.tensor import ShapeMismatchError
+    q = rand_bshd(1, 300, 2, 64, torch.float16, 85)
+    k = rand_bshd(1, 600, 2, 64, torch.float16, 86)
+    part, n = fs().fwd_partial(q, k, k)
+    with pytest.raises(ShapeMismatchError, match="partial"):
+        fs().combine(part[:-1], n, q)
+    with pytest.raises(ShapeMismatchError, match="partial"):
+        fs().combine(part, n + 1, q)
+    with pytest.raises(ShapeMismatchError, match="out tensor"):
+        fs().combine(part, n, q, out=torch.empty((1, 299, 2, 64), dtype=torch.float16, device="cuda"))
+    o = fs().combine(part, n, q)
+    assert torch.equal(o, fs().fwd(q, k, k, kv_splits=1))
+
+
 def test_cuda_graph_capture_and_replay():
     # fs_fwd is capturable (memset node + kernel node); replays see new input data
     q = rand_bshd(2, 300, 4, 128, torch.bfloat16, 90)
