@@ -296,7 +296,21 @@ def context_baselines(cfg, q, k, v, device):
     def sdpa():
         F.scaled_dot_product_attention(qb.transpose(1, 2), kb.transpose(1, 2), vb.transpose(1, 2))
 
-    for name, fn in (("torch_eager_spherical", eager), ("sdpa_softmax", sdpa)):
+    fns = [("torch_eager_spherical", eager), ("sdpa_softmax", sdpa)]
+    try:  # each SDPA backend separately, so the line says which one the default picked
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        def pinned(be):
+            def run():
+                with sdpa_kernel([be]):
+                    sdpa()
+            return run
+        for be in (SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION):
+            fns.append((f"sdpa_softmax_{be.name.lower()}", pinned(be)))
+    except ImportError:
+        pass
+
+    for name, fn in fns:
         try:
             fn()
             torch.cuda.synchronize()
