@@ -124,6 +124,36 @@ int64_t fs_partial_floats(const fs_fwd_params *p);
    split / context-parallel path.  Async on `stream`. */
 fs_status fs_combine(const fs_fwd_params *p, int32_t n_parts, fs_stream_t stream);
 
+/* Context parallelism over peer memory (NVLink P2P / CUDA IPC) instead of an all-reduce
+   (streaming.py:122-128 merge; Lemma 1).  `world` ranks hold disjoint K/V
+   shards of the same (b, h) streams and all of Q; query positions are owned in ranges of
+   rows_per_rank (owner of position n = n / rows_per_rank).  fs_fwd_peer runs this rank's K/V
+   shard and its epilogue stores every row's partial (numerator, z) straight into the OWNER's
+   workspace, slot `rank`: workspace = numerators [world][B][H][rows_per_rank][Dk] then
+   z [world][B][H][rows_per_rank] (fs_peer_floats floats; Dk as for `partial`).  Once every
+   rank's fs_fwd_peer has completed (the caller synchronises its stream and barriers),
+   fs_combine_peer normalises this rank's positions [rank*R, rank*R + R) into p->o and sets the
+   bad-row key.  No collective library call on the data path. */
+typedef struct fs_peer_params {
+  int32_t world;              /* ranks */
+  int32_t rank;               /* this rank: its slot in every owner's workspace */
+  int32_t rows_per_rank;      /* query positions owned per rank; world * R >= seqlen_q */
+  int32_t reserved0;          /* must be 0 */
+  float *const *peer_partial; /* device array [world] of the ranks' workspaces (peer-mapped) */
+  float *local_partial;       /* this rank's workspace (== peer_partial[rank] on the device) */
+} fs_peer_params;
+
+int64_t fs_peer_floats(const fs_fwd_params *p, const fs_peer_params *peer);
+fs_status fs_fwd_peer(const fs_fwd_params *p, const fs_peer_params *peer, fs_stream_t stream);
+fs_status fs_combine_peer(const fs_fwd_params *p, const fs_peer_params *peer, fs_stream_t stream);
+
+/* Peer workspaces: cudaMalloc + cudaIpcGetMemHandle (64-byte handle out), open / close a peer's
+   handle (lazy peer access), free. */
+fs_status fs_ipc_malloc(int64_t bytes, void **ptr, void *handle64);
+fs_status fs_ipc_open(const void *handle64, void **ptr);
+fs_status fs_ipc_close(void *ptr);
+fs_status fs_ipc_free(void *ptr);
+
 /* Thread-local text of the last non-FS_OK status. */
 const char *fs_last_error(void);
 

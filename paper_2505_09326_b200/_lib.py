@@ -21,7 +21,8 @@ FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
 
 # every symbol include/flashsign.h declares
 EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version", "fs_kv_splits", "fs_partial_floats",
-                    "fs_combine")
+                    "fs_combine", "fs_peer_floats", "fs_fwd_peer", "fs_combine_peer", "fs_ipc_malloc", "fs_ipc_open",
+                    "fs_ipc_close", "fs_ipc_free")
 
 
 class FsFwdParams(ctypes.Structure):
@@ -63,6 +64,21 @@ class FsFwdParams(ctypes.Structure):
     ]
 
 
+class FsPeerParams(ctypes.Structure):
+    """Mirror of ``fs_peer_params`` (include/flashsign.h)."""
+
+    _fields_ = [
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("rows_per_rank", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
+        ("peer_partial", ctypes.c_void_p),
+        ("local_partial", ctypes.c_void_p),
+    ]
+
+
+IPC_HANDLE_BYTES = 64
+
 _lock = threading.Lock()
 _lib = None
 
@@ -95,6 +111,21 @@ def load() -> ctypes.CDLL:
             lib.fs_partial_floats.restype = ctypes.c_int64
             lib.fs_combine.argtypes = [ctypes.POINTER(FsFwdParams), ctypes.c_int32, ctypes.c_void_p]
             lib.fs_combine.restype = ctypes.c_int
+            pp, fp = ctypes.POINTER(FsPeerParams), ctypes.POINTER(FsFwdParams)
+            lib.fs_peer_floats.argtypes = [fp, pp]
+            lib.fs_peer_floats.restype = ctypes.c_int64
+            lib.fs_fwd_peer.argtypes = [fp, pp, ctypes.c_void_p]
+            lib.fs_fwd_peer.restype = ctypes.c_int
+            lib.fs_combine_peer.argtypes = [fp, pp, ctypes.c_void_p]
+            lib.fs_combine_peer.restype = ctypes.c_int
+            lib.fs_ipc_malloc.argtypes = [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]
+            lib.fs_ipc_malloc.restype = ctypes.c_int
+            lib.fs_ipc_open.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+            lib.fs_ipc_open.restype = ctypes.c_int
+            lib.fs_ipc_close.argtypes = [ctypes.c_void_p]
+            lib.fs_ipc_close.restype = ctypes.c_int
+            lib.fs_ipc_free.argtypes = [ctypes.c_void_p]
+            lib.fs_ipc_free.restype = ctypes.c_int
             _lib = lib
     return _lib
 

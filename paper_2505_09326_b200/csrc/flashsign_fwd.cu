@@ -152,6 +152,10 @@ struct KParams {
   int32_t n_kv_tiles;      // ceil(seqlen_kv / BN)
   float* part_num;         // non-NULL: write fp32 partial numerators [S][B][H][Nq][D] here instead of O
   float* part_z;           //           and partial z [S][B][H][Nq] (no normalisation, no bad-row check)
+  // context parallelism over peer memory (fs_fwd_peer): partials go straight to the owner of
+  // the query position, n / peer_rows, into its workspace slot peer_rank
+  float* const* peer;      // device array [peer_world] of the ranks' workspaces (NULL: off)
+  int32_t peer_world, peer_rank, peer_rows;
 };
 
 template <int IN>
@@ -877,19 +881,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const int row = tc.qblk * (NQT * BM) + t * BM + r;
         const bool live = row < p.seqlen_q;
-        const bool partial = p.part_num != nullptr;
+        const bool partial = p.part_num != nullptr || p.peer != nullptr;
         const float den = NORM == FS_NORM_SIGNED_L1 ? zr + p.eps : sqrtf(zr + p.eps);
         // partial mode: the unnormalised numerator (the combine step divides by b(sum z + eps))
         float mul = partial ? p.out_mul : __fdiv_rn(p.out_mul, den);
         // partial row index: ((split * B + batch) * H + head) * Nq + row
         const int64_t prow =
             ((static_cast<int64_t>(tc.split) * p.n_batch + tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
+        // where this row's partial goes: the local workspace, or (peer mode) slot peer_rank of the
+        // owner's workspace -- numerators [world][B][H][Rn][D] then z [world][B][H][Rn]
+        float* num_dst = p.part_num + prow * D;
+        float* z_dst = p.part_z + prow;
+        if (p.peer != nullptr && live) {
+          const int owner = row / p.peer_rows;
+          const int64_t rows_slot = static_cast<int64_t>(p.n_batch) * p.heads_q * p.peer_rows;
+          const int64_t loc = p.peer_rank * rows_slot +
+                              (static_cast<int64_t>(tc.batch) * p.heads_q + tc.head) * p.peer_rows +
+                              (row - owner * p.peer_rows);
+          float* base = p.peer[owner];
+          num_dst = base + loc * D;
+          z_dst = base + static_cast<int64_t>(p.peer_world) * rows_slot * D + loc;
+        }
         // row status once O's first columns are in: FP16 P overflow (inf) makes every O element
         // non-finite, so one column tells; it is reported as z = +inf like a saturated FP8 P
         auto finish_row = [&](bool ovf_o) {
           const float z_report = ovf_o ? __int_as_float(0x7f800000) : zr;
           const bool bad = !partial && (ovf_o || !(den > 0.f) || isinf(den));
-          if (partial && live) p.part_z[prow] = z_report;
+          if (partial && live) *z_dst = z_report;
           if (live && bad && p.bad_key != nullptr) {
             const uint64_t lin = (static_cast<uint64_t>(tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
             atomicMin(reinterpret_cast<unsigned long long*>(p.bad_key),
@@ -932,7 +950,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = (mul == 0.f) ? 0.f : __uint_as_float(acc[i]) * mul;
           if (partial) {
-            if (live) store32<FS_F32>(p.part_num + prow * D + c * 32, v, c * 32, D);
+            if (live) store32<FS_F32>(num_dst + c * 32, v, c * 32, D);
           } else if (live && c * 32 < p.head_dim) {
             store32<OUT>(dst + c * 32, v, c * 32, p.head_dim);
           }
@@ -941,6 +959,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
 
+  // peer mode: the partials went to other GPUs' memory; make them visible system-wide before exit
+  if (p.peer != nullptr && warp >= WARP_EPI) __threadfence_system();
   ptx::tc_fence_before();
   if constexpr (C::P2) {
     ptx::cluster_sync();  // both CTAs are done with the pair's TMEM and with each other's barriers
@@ -961,6 +981,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ====================================================================== host
 
 static thread_local std::string g_last_error;
+// set by fs_fwd_peer around its fs_fwd call: route the partials to the owners' workspaces
+static thread_local const fs_peer_params* g_peer = nullptr;
 
 static fs_status fail(fs_status st, const std::string& msg) {
   g_last_error = msg;
@@ -1143,6 +1165,94 @@ static fs_status combine(const fs_fwd_params* p, int n_parts, cudaStream_t strea
   return FS_OK;
 }
 
+// Peer-mode merge (context parallelism over peer memory): this rank owns query positions
+// [n0, n0 + nr) of every (b, h); its workspace holds the world ranks' partials of them,
+// numerators [world][B][H][Rn][DK] then z [world][B][H][Rn].  O = sum num / b(sum z + eps)
+// into O[b, n, h, :], plus the bad-row key (linear row (b*H + h)*Nq + n).  One thread per 4 columns.
+template <int OUT, int NORM, int DK>
+__global__ void __launch_bounds__(256) flashsign_combine_peer_kernel(const float* __restrict__ ws, int world,
+                                                                     int batch, int heads, int seqlen_q, int rn,
+                                                                     int n0, int nr, void* o, int64_t o_sb,
+                                                                     int64_t o_sn, int64_t o_sh, int head_dim,
+                                                                     float eps, uint64_t* bad_key) {
+  constexpr int TPR = DK / 4;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r = gid / TPR;  // (b*H + h)*nr + i
+  const int c4 = static_cast<int>(gid % TPR) * 4;
+  if (r >= static_cast<int64_t>(batch) * heads * nr) return;
+  const int i = static_cast<int>(r % nr);
+  const int64_t bh = r / nr;
+  const int64_t slot_rows = static_cast<int64_t>(batch) * heads * rn;
+  const int64_t loc = bh * rn + i;
+  float z = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < world; ++s) {
+    z += ws[static_cast<int64_t>(world) * slot_rows * DK + s * slot_rows + loc];
+    const float4 a = *reinterpret_cast<const float4*>(ws + (s * slot_rows + loc) * DK + c4);
+    acc.x += a.x;
+    acc.y += a.y;
+    acc.z += a.z;
+    acc.w += a.w;
+  }
+  const int n = n0 + i;
+  const float den = NORM == FS_NORM_SIGNED_L1 ? z + eps : sqrtf(z + eps);
+  if ((!(den > 0.f) || isinf(den)) && c4 == 0 && bad_key != nullptr) {
+    const uint64_t lin = static_cast<uint64_t>(bh) * seqlen_q + n;
+    atomicMin(reinterpret_cast<unsigned long long*>(bad_key),
+              static_cast<unsigned long long>((lin << 32) | __float_as_uint(z)));
+  }
+  if (c4 >= head_dim) return;
+  const float inv = __fdiv_rn(1.0f, den);
+  const int h = static_cast<int>(bh % heads);
+  const int64_t b = bh / heads;
+  using OT = typename OutT<OUT>::T;
+  OT* dst = reinterpret_cast<OT*>(o) + b * o_sb + static_cast<int64_t>(n) * o_sn + h * o_sh + c4;
+  const float v0 = acc.x * inv, v1 = acc.y * inv, v2 = acc.z * inv, v3 = acc.w * inv;
+  if constexpr (OUT == FS_F32) {
+    *reinterpret_cast<float4*>(dst) = make_float4(v0, v1, v2, v3);
+  } else {
+    uint2 w;
+    w.x = pack2<OUT>(v0, v1);
+    w.y = pack2<OUT>(v2, v3);
+    *reinterpret_cast<uint2*>(dst) = w;
+  }
+}
+
+template <int DK>
+static fs_status combine_peer(const fs_fwd_params* p, const fs_peer_params* pp, cudaStream_t stream) {
+  const int n0 = pp->rank * pp->rows_per_rank;
+  const int nr = std::max(0, std::min(pp->rows_per_rank, p->seqlen_q - n0));
+  const int64_t rows = (int64_t)p->batch * p->heads_q * nr;
+  if (rows == 0) return FS_OK;
+  const int64_t threads = rows * (DK / 4);
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  auto go = [&](auto kern) {
+    kern<<<blocks, 256, 0, stream>>>(pp->local_partial, pp->world, p->batch, p->heads_q, p->seqlen_q,
+                                     pp->rows_per_rank, n0, nr, p->o, p->o_stride[0], p->o_stride[1],
+                                     p->o_stride[2], p->head_dim, p->eps, p->bad_key);
+  };
+  const bool l1 = p->normalizer == FS_NORM_SIGNED_L1;
+  switch (p->out_dtype) {
+    case FS_F32:
+      l1 ? go(flashsign_combine_peer_kernel<FS_F32, FS_NORM_SIGNED_L1, DK>)
+         : go(flashsign_combine_peer_kernel<FS_F32, FS_NORM_SPHERICAL, DK>);
+      break;
+    case FS_BF16:
+      l1 ? go(flashsign_combine_peer_kernel<FS_BF16, FS_NORM_SIGNED_L1, DK>)
+         : go(flashsign_combine_peer_kernel<FS_BF16, FS_NORM_SPHERICAL, DK>);
+      break;
+    case FS_F16:
+      l1 ? go(flashsign_combine_peer_kernel<FS_F16, FS_NORM_SIGNED_L1, DK>)
+         : go(flashsign_combine_peer_kernel<FS_F16, FS_NORM_SPHERICAL, DK>);
+      break;
+    default:
+      return fail(FS_ERR_DTYPE, "out_dtype must be FS_F32, FS_BF16 or FS_F16");
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("combine_peer launch: ") + cudaGetErrorString(e));
+  return FS_OK;
+}
+
 template <int IN, int D, int OUT, int NORM, bool KS>
 static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   using C = Cfg<IN, D, KS>;
@@ -1203,6 +1313,15 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
   kp.part_num = partial ? p->partial : nullptr;
   kp.part_z = partial ? p->partial + (int64_t)sp.splits * rows * D : nullptr;
+  kp.peer = nullptr;
+  kp.peer_world = kp.peer_rank = kp.peer_rows = 0;
+  if (g_peer != nullptr) {
+    kp.part_num = kp.part_z = nullptr;
+    kp.peer = g_peer->peer_partial;
+    kp.peer_world = g_peer->world;
+    kp.peer_rank = g_peer->rank;
+    kp.peer_rows = g_peer->rows_per_rank;
+  }
   int grid = (int)std::min<int64_t>(n_tiles * CL, (num_sms() / CL) * CL);
   if (grid <= 0) return fail(FS_ERR_CUDA, "no SMs reported for the current device");
   cudaError_t e;
@@ -1317,6 +1436,85 @@ fs_status fs_combine(const fs_fwd_params* p, int32_t n_parts, fs_stream_t stream
   return kernel_d(p) == 128 ? combine<128>(p, n_parts, stream) : combine<64>(p, n_parts, stream);
 }
 
+static fs_status check_peer(const fs_fwd_params* p, const fs_peer_params* pp) {
+  using namespace fs;
+  if (!p || !pp) return fail(FS_ERR_CONFIG, "null params");
+  if (pp->world < 1 || pp->rank < 0 || pp->rank >= pp->world)
+    return fail(FS_ERR_CONFIG, "peer: need 0 <= rank < world");
+  if (pp->rows_per_rank < 1 || (int64_t)pp->rows_per_rank * pp->world < p->seqlen_q)
+    return fail(FS_ERR_CONFIG, "peer: rows_per_rank * world must cover seqlen_q");
+  if (!pp->peer_partial || !pp->local_partial || (reinterpret_cast<uintptr_t>(pp->local_partial) & 15u))
+    return fail(FS_ERR_CONFIG, "peer: peer_partial (device array) and a 16-byte aligned local_partial are required");
+  return FS_OK;
+}
+
+int64_t fs_peer_floats(const fs_fwd_params* p, const fs_peer_params* pp) {
+  if (!p || !pp || pp->world < 1 || pp->rows_per_rank < 1) return 0;
+  return (int64_t)pp->world * p->batch * p->heads_q * pp->rows_per_rank * (fs::kernel_d(p) + 1);
+}
+
+fs_status fs_fwd_peer(const fs_fwd_params* p, const fs_peer_params* pp, fs_stream_t stream) {
+  fs_status st = check_peer(p, pp);
+  if (st != FS_OK) return st;
+  fs_fwd_params q = *p;
+  q.kv_splits = 1;
+  q.partial_only = 1;
+  q.partial = nullptr;
+  q.bad_key = nullptr;  // partials carry z; the owner's combine flags bad rows
+  fs::g_peer = pp;
+  st = fs_fwd(&q, stream);
+  fs::g_peer = nullptr;
+  return st;
+}
+
+fs_status fs_combine_peer(const fs_fwd_params* p, const fs_peer_params* pp, fs_stream_t stream_) {
+  using namespace fs;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  fs_status st = check_peer(p, pp);
+  if (st != FS_OK) return st;
+  if (p->normalizer != FS_NORM_SPHERICAL && p->normalizer != FS_NORM_SIGNED_L1)
+    return fail(FS_ERR_CONFIG, "normalizer must be FS_NORM_SPHERICAL or FS_NORM_SIGNED_L1");
+  if (!(p->eps >= 0.0f) || !std::isfinite(p->eps)) return fail(FS_ERR_CONFIG, "denom_epsilon must be finite and >= 0");
+  if (p->bad_key) {
+    cudaError_t e = cudaMemsetAsync(p->bad_key, 0xFF, sizeof(uint64_t), stream);
+    if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
+  }
+  return kernel_d(p) == 128 ? combine_peer<128>(p, pp, stream) : combine_peer<64>(p, pp, stream);
+}
+
+fs_status fs_ipc_malloc(int64_t bytes, void** ptr, void* handle64) {
+  using namespace fs;
+  if (!ptr || !handle64 || bytes <= 0) return fail(FS_ERR_CONFIG, "fs_ipc_malloc: bad arguments");
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle64), *ptr);
+  if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("fs_ipc_malloc: ") + cudaGetErrorString(e));
+  return FS_OK;
+}
+
+fs_status fs_ipc_open(const void* handle64, void** ptr) {
+  using namespace fs;
+  if (!ptr || !handle64) return fail(FS_ERR_CONFIG, "fs_ipc_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("fs_ipc_open: ") + cudaGetErrorString(e));
+  return FS_OK;
+}
+
+fs_status fs_ipc_close(void* ptr) {
+  using namespace fs;
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("fs_ipc_close: ") + cudaGetErrorString(e));
+  return FS_OK;
+}
+
+fs_status fs_ipc_free(void* ptr) {
+  using namespace fs;
+  cudaError_t e = cudaFree(ptr);
+  if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("fs_ipc_free: ") + cudaGetErrorString(e));
+  return FS_OK;
+}
+
 int fs_query_tile(int head_dim, fs_dtype dt, int* bm, int* bn) {
   if (!bm || !bn || head_dim < 1 || head_dim > 128) return 1;
   if (dt != FS_F16 && dt != FS_BF16 && dt != FS_E4M3) return 1;
@@ -1368,7 +1566,8 @@ fs_status fs_fwd(const fs_fwd_params* p, fs_stream_t stream_) {
       return fail(FS_ERR_UNSUPPORTED, "key_scale_stride must be >= seqlen_kv and a multiple of 4 elements");
   }
   if (p->kv_splits < 0) return fail(FS_ERR_CONFIG, "kv_splits must be >= 0");
-  if ((split_plan(p).splits > 1 || p->partial_only) && (p->partial == nullptr || !aligned16(p->partial)))
+  if (g_peer == nullptr && (split_plan(p).splits > 1 || p->partial_only) &&
+      (p->partial == nullptr || !aligned16(p->partial)))
     return fail(FS_ERR_CONFIG, "kv_splits > 1 / partial_only need a 16-byte aligned `partial` workspace of "
                                "fs_partial_floats(p) floats");
   if (p->bad_key) {

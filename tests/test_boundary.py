@@ -52,18 +52,40 @@ def test_library_is_sm100a_with_tcgen05():
     assert "HMMA" not in re.sub(r"UTC[HQ]MMA", "", sass)  # no legacy mma.sync path
 
 
-def test_struct_layout_matches_header(tmp_path):
-    fields = [f[0] for f in _lib.FsFwdParams._fields_]
+@pytest.mark.parametrize("cname,cls", [("fs_fwd_params", _lib.FsFwdParams), ("fs_peer_params", _lib.FsPeerParams)])
+def test_struct_layout_matches_header(tmp_path, cname, cls):
+    fields = [f[0] for f in cls._fields_]
     prog = tmp_path / "layout.c"
-    body = "\n".join(f'printf("{f} %zu\\n", offsetof(fs_fwd_params, {f}));' for f in fields)
+    body = "\n".join(f'printf("{f} %zu\\n", offsetof({cname}, {f}));' for f in fields)
     prog.write_text(f'#include <stdio.h>\n#include <stddef.h>\n#include "{HEADER}"\nint main(void){{\n'
-                    f'printf("size %zu\\n", sizeof(fs_fwd_params));\n{body}\nreturn 0;}}\n')
+                    f'printf("size %zu\\n", sizeof({cname}));\n{body}\nreturn 0;}}\n')
     exe = tmp_path / "layout"
     subprocess.run(["gcc", "-std=c99", str(prog), "-o", str(exe)], check=True)
     got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
-    assert int(got["size"]) == ctypes.sizeof(_lib.FsFwdParams)
+    assert int(got["size"]) == ctypes.sizeof(cls)
     for f in fields:
-        assert int(got[f]) == getattr(_lib.FsFwdParams, f).offset, f
+        assert int(got[f]) == getattr(cls, f).offset, f
+
+
+def test_peer_validation_without_gpu():
+    # fs_fwd_peer / fs_combine_peer reject bad rank layouts before touching the device
+    lib = _lib.load()
+    prm = _params()
+    for world, rank, rows in ((0, 0, 64), (2, 2, 64), (2, 0, 63), (2, -1, 64)):
+        pp = _lib.FsPeerParams()
+        pp.world, pp.rank, pp.rows_per_rank = world, rank, rows
+        pp.peer_partial, pp.local_partial = 1 << 20, 1 << 20
+        assert lib.fs_fwd_peer(ctypes.byref(prm), ctypes.byref(pp), None) == _lib.FS_ERR_CONFIG
+        assert lib.fs_combine_peer(ctypes.byref(prm), ctypes.byref(pp), None) == _lib.FS_ERR_CONFIG
+    pp = _lib.FsPeerParams()
+    pp.world, pp.rank, pp.rows_per_rank = 2, 1, 64
+    assert lib.fs_fwd_peer(ctypes.byref(prm), ctypes.byref(pp), None) == _lib.FS_ERR_CONFIG  # no workspaces
+    pp.peer_partial, pp.local_partial = 1 << 20, 1 << 20
+    # numerators [2][B=1][H=4][64][64] + z [2][1][4][64]
+    assert lib.fs_peer_floats(ctypes.byref(prm), ctypes.byref(pp)) == 2 * 4 * 64 * 65
+    from paper_2505_09326_b200.peer import peer_rows
+    assert [peer_rows(10, 3, r) for r in range(3)] == [(0, 4), (4, 8), (8, 10)]
+    assert [peer_rows(2, 3, r) for r in range(3)] == [(0, 1), (1, 2), (2, 2)]
 
 
 def _params(**kw):
