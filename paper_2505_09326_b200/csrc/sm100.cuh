@@ -118,12 +118,18 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar_addr, uint32_t p
   return ok != 0;
 }
 
+#ifndef FS_WATCHDOG_NS
+#define FS_WATCHDOG_NS 30000000000ull
+#endif
+
 #ifndef FS_WAIT_HINT
 #define FS_WAIT_HINT 0  // 0: system-default try_wait time limit
 #endif
 
 // Blocking wait on the phase with the given parity.  A watchdog turns a
-// protocol bug into a trapped launch (cudaErrorLaunchFailure) after ~4 s
+// protocol bug into a trapped launch (cudaErrorLaunchFailure) after FS_WATCHDOG_NS (30 s: the
+// longest legitimate wait is the epilogue's for one whole work tile, ~9 s for a single (b, h)
+// stream of 2^31 keys run unsplit)
 // instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
@@ -132,7 +138,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!(FS_WAIT_HINT ? mbar_try_wait_hint(a, parity, FS_WAIT_HINT) : mbar_try_wait(a, parity))) {
     // no printf here: a call would make every waiting role spill its live registers
-    if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+    if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > FS_WATCHDOG_NS) __trap();
   }
 }
 
@@ -163,7 +169,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   const uint64_t t0 = globaltimer();
   uint32_t spins = 0;
   while (!probe()) {
-    if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+    if ((++spins & 0x3FFu) == 0 && globaltimer() - t0 > FS_WATCHDOG_NS) __trap();
   }
 }
 
