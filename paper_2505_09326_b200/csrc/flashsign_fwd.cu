@@ -15,12 +15,13 @@
 //                               issued once all of P_t is in TMEM; every lane runs the
 //                               issue code, the elected lane's predicate makes it the issuer
 //   warp 2       TMEM allocator (512 columns: S_0, S_1, O_0, O_1 [, second O set when d=64])
-//   warps 4-11   norm, tile 0   warp (column half h, lane quarter) owns 32 rows x 64 scores of
+//   warps 4-11   norm, tile 0   warp (column half h, lane quarter) owns 32 rows x BN/2 scores of
 //                               S_0: z += a2(s) (packed FFMA2/FADD2, registers), P = cvt(s) ->
 //                               TMEM in place (first columns of its own half of S)
 //   warps 12-19  norm, tile 1   same for S_1, ping-ponging with tile 0
 //   warps 20-23  epilogue WG    O_t -> registers (frees TMEM for the next work tile),
-//                               O = acc * c / b(z + eps) -> global, or fp32 partials (split K/V)
+//                               O = acc * c / b(z + eps) -> global, or fp32 partials (split K/V;
+//                               peer mode: straight into the owning rank's workspace)
 //
 // CTAs run in clusters of two on adjacent query blocks of the same (batch, head, K/V range).
 // d=128 16-bit (Cfg::P2): the pair is one tcgen05 CTA pair -- the rank-0 CTA issues M=256
