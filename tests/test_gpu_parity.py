@@ -454,6 +454,27 @@ def test_host_pipeline_equals_device_path():
         HostPipeline(0, chunk=1, q_split=3).run(qh, kh, vh, oh)
 
 
+def test_host_pipeline_with_multiplicities_and_fp8():
+    from paper_2505_09326_b200.pipeline import HostPipeline
+    q = rand_bshd(3, 600, 4, 64, torch.float16, 53)
+    k = rand_bshd(3, 500, 2, 64, torch.float16, 54)
+    v = rand_bshd(3, 500, 2, 64, torch.float16, 55)
+    g = torch.Generator(device="cuda").manual_seed(56)
+    m = torch.randint(0, 6, (3, 500), generator=g, device="cuda").float()
+    ref = fs().fwd(q, k, v, eps=1e-6, key_scale=m)
+    qh, kh, vh, mh = (t.cpu().pin_memory() for t in (q, k, v, m))
+    oh = torch.empty(q.shape, dtype=torch.float16, pin_memory=True)
+    for chunk, qs in ((1, None), (2, 2)):
+        HostPipeline(0, chunk=chunk, q_split=qs).run(qh, kh, vh, oh, eps=1e-6, key_scale=mh)
+        assert torch.equal(oh, ref.cpu()), (chunk, qs)
+    # e4m3 inputs, bf16 output
+    q8, k8, v8 = (t.to(torch.float8_e4m3fn) for t in (q, k, v))
+    ref8 = fs().fwd(q8, k8, v8, out_dtype=torch.bfloat16)
+    o8 = torch.empty(q.shape, dtype=torch.bfloat16, pin_memory=True)
+    HostPipeline(0).run(q8.cpu().pin_memory(), k8.cpu().pin_memory(), v8.cpu().pin_memory(), o8)
+    assert torch.equal(o8, ref8.cpu())
+
+
 # ------------------------------------------------------------------ SIGNED_L1 and fused key multiplicities
 
 # signed_l1 outputs are weighted means (weights |s|/sum|s|), so they are O(1/sqrt(N)) and the
