@@ -117,6 +117,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_PV_TRIM
 #define FS_PV_TRIM 1  // skip the PV K-steps past the end of the sequence on a ragged last K/V tile
 #endif
+#ifndef FS_CARRY
+#define FS_CARRY 1  // double-buffered Q: a work tile's last PV_1 is issued after the next tile's first QK_0
+#endif
 #ifndef FS_P2_NQB2
 #define FS_P2_NQB2 0  // CTA pairs at d=128: double-buffer Q (fewer ring slots)
 #endif
@@ -249,6 +252,10 @@ struct Cfg {
   // each half's norm starts one half-MMA earlier and ends one half-MMA later:
   // the norm window grows from 2 to 2.5 MMAs.
   static constexpr bool SPLIT = FS_SPLITS && !P2 && NWT == 8;
+  // With the next work tile's Q already resident (NQB = 2), the issue order runs on across the
+  // tile boundary: ... QK1(L-1) PV0(L-1) | QK0'(0) PV1(L-1) QK1'(0) PV0'(0) ..., so the last and
+  // first norm steps of a tile keep their two-MMA window too.
+  static constexpr bool CARRY = FS_CARRY && NQB == 2 && !P2;
   static constexpr int PV_STEPS = BN / TR::KSTEP;
   static constexpr uint32_t COL_S0 = 0;
   static constexpr uint32_t COL_O0 = NSB * BN;
@@ -561,6 +568,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       {
       uint32_t kv_i = 0;                 // ring position of this work tile's K_0
       uint32_t p_use[NQT] = {0u, 0u};    // completed phases of p_full[t]
+      // the previous work tile's last PV_1, carried over the tile boundary (Cfg::CARRY)
+      bool pend = false;
+      uint32_t pend_slot = 0, pend_o_use = 0;
+      int pend_j = 0, pend_ob = 0, pend_kb0 = 0;
       int it = 0;
       for (int tile = tile0; tile < p.n_tiles; tile += tstride, ++it) {
         const int qb = it % C::NQB;
@@ -592,16 +603,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         };
         // O_t += P_t V_j once all of P_t is in TMEM (one hand-off per tile: every extra
         // barrier round trip on the issuing warp costs more than it overlaps, measured)
-        auto pv = [&](int t, uint32_t slot, int j) {
+        // (ob_, o_use_, kb0_: the work tile the PV belongs to -- the previous one for a carried PV_1)
+        auto pv = [&](int t, uint32_t slot, int j, int ob_, uint32_t o_use_, int kb0_) {
           if (j == 0) {
             if constexpr (C::P2)
-              ptx::mbar_wait_cluster(&bars->o_empty[t][ob], (o_use & 1u) ^ 1u);
+              ptx::mbar_wait_cluster(&bars->o_empty[t][ob_], (o_use_ & 1u) ^ 1u);
             else
-              ptx::mbar_wait(&bars->o_empty[t][ob], (o_use & 1u) ^ 1u);
+              ptx::mbar_wait(&bars->o_empty[t][ob_], (o_use_ & 1u) ^ 1u);
           }
           const uint64_t b0 = v_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
           const uint32_t a_tmem = tmem + C::COL_S0 + t * BN;
-          const uint32_t d_tmem = tmem + C::COL_O0 + (ob * NQT + t) * D;
+          const uint32_t d_tmem = tmem + C::COL_O0 + (ob_ * NQT + t) * D;
           auto wait_p = [&](int h) {
 #if FS_PROF
             const long long tw0 = clock64();
@@ -635,7 +647,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           };
           // keys of this K/V tile inside the sequence: on a ragged last tile the K-steps past them
           // would multiply P = 0 (zero-filled K rows) with zero-filled V rows -- not issued
-          const int keys_left = p.seqlen_kv - (tcm.kb0 + j) * BN;
+          const int keys_left = p.seqlen_kv - (kb0_ + j) * BN;
           if (FS_PV_TRIM && keys_left < BN) {
             const int n_steps = (keys_left + TR::KSTEP - 1) / TR::KSTEP;
 #pragma unroll 1
@@ -683,20 +695,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           qk_signal(0);
           if (j == L - 1) signal(&bars->q_empty[0][qb]);
           if (j > 0) {
-            pv(1, prev_v_slot, j - 1);
+            pv(1, prev_v_slot, j - 1, ob, o_use, tcm.kb0);
             kv_release(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
+          } else if (C::CARRY && pend) {
+            pv(1, pend_slot, pend_j, pend_ob, pend_o_use, pend_kb0);
+            kv_release(&bars->kv_empty[C::kv_bar(pend_slot)]);
+            signal(&bars->o_full[1][pend_ob]);
+            pend = false;
           }
           qk_signal(1);
           if (!C::KV1) kv_release(&bars->kv_empty[k_slot]);  // KV1: freed with V after PV1
           if (j == L - 1) signal(&bars->q_empty[1][qb]);
           if (!C::KV1) ptx::mbar_wait(&bars->kv_full[v_slot], (v_idx / C::STAGES) & 1u);
-          pv(0, v_slot, j);
+          pv(0, v_slot, j, ob, o_use, tcm.kb0);
           if (j == L - 1) signal(&bars->o_full[0][ob]);
           prev_v_slot = v_slot;
         }
-        pv(1, prev_v_slot, L - 1);
-        kv_release(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
-        signal(&bars->o_full[1][ob]);
+        if (C::CARRY && tile + tstride < p.n_tiles) {
+          pend = true;
+          pend_slot = prev_v_slot;
+          pend_j = L - 1;
+          pend_ob = ob;
+          pend_o_use = o_use;
+          pend_kb0 = tcm.kb0;
+        } else {
+          pv(1, prev_v_slot, L - 1, ob, o_use, tcm.kb0);
+          kv_release(&bars->kv_empty[C::kv_bar(prev_v_slot)]);
+          signal(&bars->o_full[1][ob]);
+        }
         kv_i += 2 * L;
       }
       }
