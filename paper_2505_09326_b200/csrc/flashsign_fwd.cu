@@ -111,9 +111,6 @@ constexpr int NQT = 2;   // Q tiles per work tile
 // SM, one issuer per pair), 2 for every configuration (d=64 / e4m3: -1 to -2 % per GHz, measured)
 #define FS_2SM 1
 #endif
-#ifndef FS_SPLITS
-#define FS_SPLITS 0  // experiment: per-CTA MMAs issue S_t as two key halves (own S-ready / P-ready barriers)
-#endif
 #ifndef FS_PV_TRIM
 #define FS_PV_TRIM 1  // skip the PV K-steps past the end of the sequence on a ragged last K/V tile
 #endif
@@ -247,11 +244,6 @@ struct Cfg {
   static constexpr int SMEM_BYTES = LAYOUT_BYTES + SLACK;
   static constexpr int QK_STEPS = ROW_BYTES / 32;                          // 32 B of K-dim per MMA
   static constexpr int MMA_M = P2 ? 2 * BM : BM;
-  // Split S hand-off (per-CTA MMAs, one norm warp per column half): QK_t is issued as two
-  // key halves, each committed to its own S-ready barrier, and PV_t consumes P half by half, so
-  // each half's norm starts one half-MMA earlier and ends one half-MMA later:
-  // the norm window grows from 2 to 2.5 MMAs.
-  static constexpr bool SPLIT = FS_SPLITS && !P2 && NWT == 8;
   // With the next work tile's Q already resident (NQB = 2), the issue order runs on across the
   // tile boundary: ... QK1(L-1) PV0(L-1) | QK0'(0) PV1(L-1) QK1'(0) PV0'(0) ..., so the last and
   // first norm steps of a tile keep their two-MMA window too.
@@ -263,15 +255,14 @@ struct Cfg {
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(PV_STEPS % 2 == 0, "P is produced in two column halves");
   static constexpr uint32_t IDESC_QK = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, MMA_M, BN);
-  static constexpr uint32_t IDESC_QKH = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, MMA_M, BN / 2);
   static constexpr uint32_t IDESC_PV = ptx::idesc_make(TR::FMT, TR::FMT, 0, 1, MMA_M, D);
 };
 
 struct Bars {
   uint64_t q_full[NQT][2], q_empty[NQT][2];
   uint64_t kv_full[16], kv_empty[16];
-  uint64_t s_full[2][2];    // per S buffer (= Q tile) [x key half when Cfg::SPLIT]
-  uint64_t p_full[2][2];    // per S buffer [x key half]: the tile's norm warps have written P
+  uint64_t s_full[2];       // per S buffer (= Q tile)
+  uint64_t p_full[2];       // per S buffer: all norm warps of the tile (both CTAs of a pair) wrote P
   uint64_t o_full[NQT][2], o_empty[NQT][2];
   uint64_t z_full[NQT][2], z_empty[NQT][2];
   uint32_t tmem_base;
@@ -385,12 +376,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 32) {
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        ptx::mbar_init(&bars->s_full[b][h], 1);
-        // 2 column halves x 4 lane quarters (x 2 CTAs); split: 4 lane quarters per half
-        ptx::mbar_init(&bars->p_full[b][h], C::SPLIT ? 4 : C::P2 ? 16 : 8);
-      }
+      ptx::mbar_init(&bars->s_full[b], 1);
+      ptx::mbar_init(&bars->p_full[b], C::P2 ? 16 : 8);  // 2 column halves x 4 lane quarters (x 2 CTAs)
     }
 #pragma unroll
     for (int t = 0; t < NQT; ++t) {
@@ -580,13 +567,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
         const TileCoord tcm = decode_tile(tile, p, rank);
         const int L = tcm.L;
-        // S_t = Q_t K^T for key half h of the tile (h < 0: all BN keys)
-        auto qk = [&](int t, uint32_t slot, int h) {
-          const uint32_t hoff = h > 0 ? h * (BN / 2) : 0;  // first key (= S column) of the half
-          const uint32_t idesc = h < 0 ? C::IDESC_QK : C::IDESC_QKH;
+        // S_t = Q_t K^T over the BN keys of the slot
+        auto qk = [&](int t, uint32_t slot) {
+          constexpr uint32_t idesc = C::IDESC_QK;
           const uint64_t a0 = q_desc + static_cast<uint32_t>(((t * C::NQB + qb) * C::Q_TILE_BYTES) >> 4);
-          const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES + hoff * 128) >> 4);
-          const uint32_t d_tmem = tmem + C::COL_S0 + t * BN + hoff;
+          const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
+          const uint32_t d_tmem = tmem + C::COL_S0 + t * BN;
 #pragma unroll
           for (int ks = 0; ks < C::QK_STEPS; ++ks) {
             const uint32_t off_a = ((ks * 32 / 128) * (BM * 128) + (ks * 32) % 128) >> 4;
@@ -614,21 +600,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint64_t b0 = v_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
           const uint32_t a_tmem = tmem + C::COL_S0 + t * BN;
           const uint32_t d_tmem = tmem + C::COL_O0 + (ob_ * NQT + t) * D;
-          auto wait_p = [&](int h) {
+          auto wait_p = [&]() {
 #if FS_PROF
             const long long tw0 = clock64();
 #endif
             if constexpr (C::P2)
-              ptx::mbar_wait_cluster(&bars->p_full[t][h], p_use[t] & 1u);
+              ptx::mbar_wait_cluster(&bars->p_full[t], p_use[t] & 1u);
             else
-              ptx::mbar_wait(&bars->p_full[t][h], p_use[t] & 1u);
+              ptx::mbar_wait(&bars->p_full[t], p_use[t] & 1u);
 #if FS_PROF
             pr_pw += clock64() - tw0;
             ++pr_pn;
 #endif
             ptx::tc_fence_after();
           };
-          wait_p(0);
+          wait_p();
           auto issue = [&](int ks, uint32_t pred) {
             const int h = ks / (C::PV_STEPS / 2), k2 = ks % (C::PV_STEPS / 2);
             // (V rows are 128 B per column block; a pair's V slot has VROW_BYTES per key)
@@ -651,17 +637,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (FS_PV_TRIM && keys_left < BN) {
             const int n_steps = (keys_left + TR::KSTEP - 1) / TR::KSTEP;
 #pragma unroll 1
-            for (int ks = 0; ks < n_steps; ++ks) {
-              if (C::SPLIT && ks == C::PV_STEPS / 2) wait_p(1);
-              issue(ks, lp);
-            }
-            if (C::SPLIT && n_steps <= C::PV_STEPS / 2) wait_p(1);  // keep the phase accounting
+            for (int ks = 0; ks < n_steps; ++ks) issue(ks, lp);
           } else {
 #pragma unroll
-            for (int ks = 0; ks < C::PV_STEPS; ++ks) {
-              if (C::SPLIT && ks == C::PV_STEPS / 2) wait_p(1);  // second key half's P
-              issue(ks, lp);
-            }
+            for (int ks = 0; ks < C::PV_STEPS; ++ks) issue(ks, lp);
           }
           ++p_use[t];
         };
@@ -682,15 +661,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
           ptx::tc_fence_after();
           auto qk_signal = [&](int t) {
-            if constexpr (C::SPLIT) {
-              qk(t, k_slot, 0);
-              signal(&bars->s_full[t][0]);
-              qk(t, k_slot, 1);
-              signal(&bars->s_full[t][1]);
-            } else {
-              qk(t, k_slot, -1);
-              signal(&bars->s_full[t][0]);
-            }
+            qk(t, k_slot);
+            signal(&bars->s_full[t]);
           };
           qk_signal(0);
           if (j == L - 1) signal(&bars->q_empty[0][qb]);
@@ -759,7 +731,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const long long tn0 = clock64();
 #endif
         const uint32_t sb = t;  // S_t's TMEM buffer; one phase per K/V tile
-        ptx::mbar_wait(&bars->s_full[sb][C::SPLIT ? hh0 : 0], s_use & 1u);
+        ptx::mbar_wait(&bars->s_full[sb], s_use & 1u);
         const uint32_t s_base = s_lane + sb * BN;
         // key multiplicities of this K/V tile ride in V_j's ring slot; that slot is released only
         // after PV_1(j), which needs this warp's P, so they stay valid while they are read here
@@ -863,9 +835,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           if (C::P2 && rank != 0)
-            ptx::mbar_arrive_cluster(lead(&bars->p_full[sb][0]));  // the pair leader issues PV
+            ptx::mbar_arrive_cluster(lead(&bars->p_full[sb]));  // the pair leader issues PV
           else
-            ptx::mbar_arrive(&bars->p_full[sb][C::SPLIT ? hh : 0]);
+            ptx::mbar_arrive(&bars->p_full[sb]);
         }
 #if FS_PROF
         pr_nc += clock64() - tn1;
