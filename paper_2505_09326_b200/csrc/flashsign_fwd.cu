@@ -350,7 +350,8 @@ __device__ __forceinline__ TileCoord decode_tile(int tile, const KParams& p, int
 
 // NORM: FS_NORM_SPHERICAL (a2 = s^2, b = sqrt) | FS_NORM_SIGNED_L1 (a2 = |s|, b = id), normalizers.py:94-117.
 // KS: per-key multiplicity scale m_j fused into the score (s_ij -> m_j s_ij), attention.py:381-388.
-template <int IN, int D, int OUT, int NORM, bool KS>
+// PEER: partials stored into the owning rank's workspace over peer memory (fs_fwd_peer).
+template <int IN, int D, int OUT, int NORM, bool KS, bool PEER>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     flashsign_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_m,
@@ -880,7 +881,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const int row = tc.qblk * (NQT * BM) + t * BM + r;
         const bool live = row < p.seqlen_q;
-        const bool partial = p.part_num != nullptr || p.peer != nullptr;
+        const bool partial = PEER || p.part_num != nullptr;
         const float den = NORM == FS_NORM_SIGNED_L1 ? zr + p.eps : sqrtf(zr + p.eps);
         // partial mode: the unnormalised numerator (the combine step divides by b(sum z + eps))
         float mul = partial ? p.out_mul : __fdiv_rn(p.out_mul, den);
@@ -891,7 +892,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // owner's workspace -- numerators [world][B][H][Rn][D] then z [world][B][H][Rn]
         float* num_dst = p.part_num + prow * D;
         float* z_dst = p.part_z + prow;
-        if (p.peer != nullptr && live) {
+        if (PEER && live) {
           const int owner = row / p.peer_rows;
           const int64_t rows_slot = static_cast<int64_t>(p.n_batch) * p.heads_q * p.peer_rows;
           const int64_t loc = p.peer_rank * rows_slot +
@@ -959,7 +960,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   // peer mode: the partials went to other GPUs' memory; make them visible system-wide before exit
-  if (p.peer != nullptr && warp >= WARP_EPI) __threadfence_system();
+  if (PEER && warp >= WARP_EPI) __threadfence_system();
   ptx::tc_fence_before();
   if constexpr (C::P2) {
     ptx::cluster_sync();  // both CTAs are done with the pair's TMEM and with each other's barriers
@@ -1252,10 +1253,10 @@ static fs_status combine_peer(const fs_fwd_params* p, const fs_peer_params* pp, 
   return FS_OK;
 }
 
-template <int IN, int D, int OUT, int NORM, bool KS>
+template <int IN, int D, int OUT, int NORM, bool KS, bool PEER = false>
 static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   using C = Cfg<IN, D, KS>;
-  auto kern = flashsign_fwd_kernel<IN, D, OUT, NORM, KS>;
+  auto kern = flashsign_fwd_kernel<IN, D, OUT, NORM, KS, PEER>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -1378,6 +1379,11 @@ static fs_status dispatch_out(const fs_fwd_params* p, cudaStream_t s) {
 template <int IN, int D>
 static fs_status dispatch_norm(const fs_fwd_params* p, cudaStream_t s) {
   const bool ks = p->key_scale != nullptr;
+  if (g_peer != nullptr) {  // peer mode: partials only (no O, so one output type), no multiplicities
+    if (ks) return fail(FS_ERR_UNSUPPORTED, "fs_fwd_peer: key_scale is not supported");
+    return p->normalizer == FS_NORM_SIGNED_L1 ? launch<IN, D, FS_F32, FS_NORM_SIGNED_L1, false, true>(p, s)
+                                              : launch<IN, D, FS_F32, FS_NORM_SPHERICAL, false, true>(p, s);
+  }
   if (p->normalizer == FS_NORM_SIGNED_L1)
     return ks ? dispatch_out<IN, D, FS_NORM_SIGNED_L1, true>(p, s) : dispatch_out<IN, D, FS_NORM_SIGNED_L1, false>(p, s);
   return ks ? dispatch_out<IN, D, FS_NORM_SPHERICAL, true>(p, s) : dispatch_out<IN, D, FS_NORM_SPHERICAL, false>(p, s);
