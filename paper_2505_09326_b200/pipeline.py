@@ -4,7 +4,7 @@
 compute dtype, e.g. bf16) and streams them through the GPU on three CUDA
 streams -- copy-in, compute, copy-out -- so PCIe transfers overlap the kernel.
 The unit of the pipeline is a query slice of one batch chunk (``chunk`` batch rows, by
-default enough for >= 32 MB of K/V per chunk): K/V of the batch
+default one row of >= 64 MB of K/V, else >= 2 rows and >= 32 MB): K/V of the batch
 chunk go over first, then its queries in ``q_split`` row slices, each launched
 as soon as it lands, so the pipeline fills after ~1/(chunks * q_split) of the
 data instead of a whole batch row and drains after one slice.  Device staging
@@ -24,9 +24,11 @@ from . import flashsign
 class HostPipeline:
     """Reusable device staging for ``fwd_host`` (two slots per tensor)."""
 
-    # batch rows per chunk when not given: enough that a chunk's K/V copies are >= 32 MB (small
-    # copies leave the link idle between them: C2 e2e +6.7 % with 2 rows of 16 MB instead of 1)
+    # batch rows per chunk when not given: one row when its K/V copies are >= 64 MB, else at least
+    # two rows and >= 32 MB (short copies leave the link idle between them; measured C2 +7 %,
+    # C5 +4 % with two rows per chunk, C3 best with one)
     KV_CHUNK_BYTES = 32 << 20
+    KV_ROW_ALONE_BYTES = 64 << 20
 
     def __init__(self, device: torch.device | int | None = None, chunk: int | None = None,
                  q_split: int | None = None):
@@ -85,7 +87,8 @@ class HostPipeline:
         if check and key_scale is not None:
             flashsign.check_key_scale(key_scale)
         row_kv = 2 * k[0].numel() * k.element_size()
-        self._c = self.chunk or max(1, min(q.shape[0], -(-self.KV_CHUNK_BYTES // max(row_kv, 1))))
+        auto = 1 if row_kv >= self.KV_ROW_ALONE_BYTES else max(2, -(-self.KV_CHUNK_BYTES // max(row_kv, 1)))
+        self._c = self.chunk or max(1, min(q.shape[0], auto))
         self._alloc(q, k, out, key_scale)
         c = self._c
         nb, nq, h = q.shape[0], q.shape[1], q.shape[2]
