@@ -19,7 +19,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q, k, v, ref, qbad, results):
+def _worker(rank, world, port, q, k, v, ref, qbad, results, norm="spherical"):
     import torch.distributed as dist
     try:
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -29,17 +29,18 @@ def _worker(rank, world, port, q, k, v, ref, qbad, results):
         qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
         lo, hi = partition.kv_shard_range(kd.shape[1], world, rank)
         out, (a, b) = peer.context_parallel_fwd_peer(qd, kd[:, lo:hi], vd[:, lo:hi], eps=1e-6,
-                                                     out_dtype=torch.float32)
+                                                     out_dtype=torch.float32, normalizer=norm)
         assert (a, b) == peer.peer_rows(q.shape[1], world, rank)
         err = float((out[:, a:b].cpu() - ref[:, a:b]).abs().max()) if b > a else 0.0
         # second call: the other workspace of the pair, and the all-gather of O
         out2, _ = peer.context_parallel_fwd_peer(qd, kd[:, lo:hi], vd[:, lo:hi], eps=1e-6,
-                                                 out_dtype=torch.float32, gather=True)
+                                                 out_dtype=torch.float32, gather=True, normalizer=norm)
         err2 = float((out2.cpu() - ref).abs().max())
         # a degenerate row (q = 0, eps = 0) is reported by the rank that owns its position only
         raised = False
         try:
-            peer.context_parallel_fwd_peer(qbad.cuda(), kd[:, lo:hi], vd[:, lo:hi], out_dtype=torch.float32)
+            peer.context_parallel_fwd_peer(qbad.cuda(), kd[:, lo:hi], vd[:, lo:hi], out_dtype=torch.float32,
+                                           normalizer=norm)
         except DegenerateDenominatorError as e:
             raised = "row 5" in str(e)
         peer.release_workspaces()
@@ -49,9 +50,11 @@ def _worker(rank, world, port, q, k, v, ref, qbad, results):
         results.put((rank, None, None, None, repr(e)))
 
 
-@pytest.mark.parametrize("world,dt,nq,nkv", [(2, torch.bfloat16, 700, 1000), (3, torch.float16, 513, 777),
-                                             (2, torch.float8_e4m3fn, 256, 300)])
-def test_context_parallel_over_peer_memory(world, dt, nq, nkv):
+@pytest.mark.parametrize("world,dt,nq,nkv,norm", [(2, torch.bfloat16, 700, 1000, "spherical"),
+                                                  (3, torch.float16, 513, 777, "spherical"),
+                                                  (2, torch.float8_e4m3fn, 256, 300, "spherical"),
+                                                  (2, torch.bfloat16, 300, 500, "signed_l1")])
+def test_context_parallel_over_peer_memory(world, dt, nq, nkv, norm):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2505_09326_b200 import flashsign
@@ -60,13 +63,14 @@ def test_context_parallel_over_peer_memory(world, dt, nq, nkv):
     q = torch.randn((2, nq, 4, d), generator=g, device="cuda").to(dt)
     k = torch.randn((2, nkv, 2, d), generator=g, device="cuda").to(dt)
     v = torch.randn((2, nkv, 2, d), generator=g, device="cuda").to(dt)
-    ref = flashsign.fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, kv_splits=1).cpu()
+    ref = flashsign.fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, kv_splits=1, normalizer=norm).cpu()
     qbad = q.clone()
     qbad[1, 5, 3] = 0
     ctx = torch.multiprocessing.get_context("spawn")
     results = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q.cpu(), k.cpu(), v.cpu(), ref, qbad.cpu(), results))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q.cpu(), k.cpu(), v.cpu(), ref, qbad.cpu(), results,
+                                               norm))
              for r in range(world)]
     for p in procs:
         p.start()
