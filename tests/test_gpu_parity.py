@@ -11,6 +11,8 @@ same quantised inputs):
 Known-answer tests whose values are exact in every dtype are checked bitwise.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -743,7 +745,10 @@ def test_16bit_descales_and_p_scale(dt):
 
 # ------------------------------------------------------------------ randomized sweep over the feature matrix
 
-def _sweep_cases(n=48, seed=2024):
+def _sweep_cases(n=None, seed=None):
+    # FS_SWEEP_N / FS_SWEEP_SEED widen the sweep for stress runs (default: 48 cases, seed 2024)
+    n = int(os.environ.get("FS_SWEEP_N", 48)) if n is None else n
+    seed = int(os.environ.get("FS_SWEEP_SEED", 2024)) if seed is None else seed
     rng = np.random.default_rng(seed)
     dts = [torch.bfloat16, torch.float16, torch.float8_e4m3fn]
     out = []
