@@ -260,3 +260,16 @@ def test_auto_splits_wave_model():
     assert fsm.auto_splits(8, 16, 16384, 16384, "cuda:0", 128) == 1       # C3: 8192 tiles
     assert fsm.auto_splits(1, 1, 16384, 16384, "cuda:0", 128) > 1         # 64 tiles on 148 SMs
     assert fsm.auto_splits(1, 1, 300, 700, "cuda:0", 128) == 1            # too few K/V tiles (6)
+
+
+def test_integration_c_snippet_compiles(tmp_path):
+    # the C example in INTEGRATION.md builds against include/flashsign.h as written
+    text = open(os.path.join(os.path.dirname(HEADER), "..", "INTEGRATION.md")).read()
+    block = text.split("C/C++ callers include the header")[1].split("```c")[1].split("```")[0]
+    lines = [ln for ln in block.splitlines() if not ln.startswith("#include")]
+    prog = tmp_path / "snippet.c"
+    prog.write_text('#include <stdio.h>\n#include <stdint.h>\n#include "' + HEADER + '"\n'
+                    "void run(void *dq, void *dk, void *dv, void *dout, uint64_t *d_bad, int B, int H, int Hkv,"
+                    " int N, fs_stream_t stream) {\n" + "\n".join(lines) + "\n}\n")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-c", str(prog), "-o", str(tmp_path / "snippet.o")],
+                   check=True)
