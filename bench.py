@@ -315,7 +315,16 @@ def context_baselines(cfg, q, k, v, device):
     def sdpa():
         F.scaled_dot_product_attention(qb.transpose(1, 2), kb.transpose(1, 2), vb.transpose(1, 2))
 
-    fns = [("torch_eager_spherical", eager), ("sdpa_softmax", sdpa)]
+    def gram():  # the O(N d^2) Gram-form identity -- a different algorithm, context only
+        hk = torch.arange(H, device=qb.device) * kb.shape[2] // H
+        qh = qb[0].float().transpose(0, 1)                       # [H, N, d]
+        kh = kb[0].float().transpose(0, 1)[hk]
+        vh = vb[0].float().transpose(0, 1)[hk]
+        kt = kh.transpose(1, 2)
+        z = (torch.bmm(qh, torch.bmm(kt, kh)) * qh).sum(-1, keepdim=True).sqrt()
+        torch.bmm(qh, torch.bmm(kt, vh)).div_(z)
+
+    fns = [("torch_eager_spherical", eager), ("sdpa_softmax", sdpa), ("gram_form_fp32_not_flashsign", gram)]
     try:  # each SDPA backend separately, so the line says which one the default picked
         from torch.nn.attention import SDPBackend, sdpa_kernel
 
@@ -340,7 +349,9 @@ def context_baselines(cfg, q, k, v, device):
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 3
-            res[name] = {"tflops": fl / ms / 1e9, "ms_per_batch_row": ms, "dtype": str(qb.dtype)}
+            res[name] = ({"ms_per_batch_row": ms, "note": "O(N d^2) identity, not the 4*N^2*d FlashSign work"}
+                         if name.startswith("gram") else
+                         {"tflops": fl / ms / 1e9, "ms_per_batch_row": ms, "dtype": str(qb.dtype)})
         except Exception as ex:  # OOM etc. recorded, as the paper did
             res[name] = {"error": f"{type(ex).__name__}: {str(ex)[:120]}"}
     return res
