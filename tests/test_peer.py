@@ -82,3 +82,33 @@ def test_context_parallel_over_peer_memory(world, dt, nq, nkv, norm):
         assert exc is None, f"rank {rank}: {exc}"
         assert err <= tol and err2 <= tol, (rank, err, err2)
         assert raised == (rank == 0), rank  # position 5 belongs to rank 0
+
+
+def test_peer_path_single_process_equals_single_pass():
+    # world 1 (no process group): the kernel stores every partial into this rank's own workspace
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2505_09326_b200 import flashsign, peer
+    g = torch.Generator(device="cuda").manual_seed(300)
+    q = torch.randn((2, 333, 4, 128), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((2, 444, 4, 128), generator=g, device="cuda").to(torch.bfloat16)
+    v = torch.randn((2, 444, 4, 128), generator=g, device="cuda").to(torch.bfloat16)
+    out, (lo, hi) = peer.context_parallel_fwd_peer(q, k, v, eps=1e-6, out_dtype=torch.float32)
+    assert (lo, hi) == (0, 333)
+    ref = flashsign.fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, kv_splits=1)
+    assert float((out - ref).abs().max()) <= 1e-5 * max(1.0, float(ref.abs().max()))
+    with pytest.raises(Exception, match="key_scale|unsupported|not supported"):
+        # multiplicities are not part of the peer path
+        from paper_2505_09326_b200 import _lib
+        import ctypes
+        prm = peer._params(q, k, v, out, 1.0, 0.0, "spherical", torch.empty(1, dtype=torch.int64, device="cuda"))
+        m = torch.ones((2, 444), device="cuda")
+        prm.key_scale, prm.key_scale_stride = m.data_ptr(), m.stride(0)
+        ws = peer.PeerWorkspace(1 << 20)
+        pp = _lib.FsPeerParams()
+        pp.world, pp.rank, pp.rows_per_rank = 1, 0, 333
+        pp.peer_partial, pp.local_partial = ws.table.data_ptr(), ws.local
+        st = _lib.load().fs_fwd_peer(ctypes.byref(prm), ctypes.byref(pp), None)
+        ws.close()
+        raise RuntimeError(_lib.last_error() if st != _lib.FS_OK else "accepted")
+    peer.release_workspaces()
