@@ -11,9 +11,15 @@ is fixed, ranks split it).  Timing: W warm-up steps, barrier +
 synchronize, CUDA events around exactly K steps on the launching stream,
 synchronize + barrier, MAX over ranks.  Rank 0 prints one JSON line.
 
-``--impl reference`` times the reference's CPU algorithm (the oracle port of
-``_streamed_tiles``, oracle/spherical.py, tile 64x64, float32) on this host's
-cores on a bounded sample of the same workload.
+``--impl reference`` times the reference's own CPU implementation -- ncstream's
+``multi_head_attention_array`` from baseline/_ref (baseline/install_ref.sh), else the
+oracle port of the same loop -- on this host's cores on a bounded sample of the same
+workload (``kind`` says which ran).
+
+Beside the device-timed value the line carries: ``e2e`` (HostPipeline, pinned host
+buffers), ``e2e_dropin`` (the reference's call pattern through the numpy drop-in API),
+``context`` (SDPA softmax / eager spherical on the full configuration, same window
+protocol), ``host_latency`` (per-call host microseconds), ``roofline``, ``cpu_baseline``.
 """
 
 from __future__ import annotations
@@ -83,7 +89,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period_s: float = 0.02):
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index, self.period = index, period_s
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
@@ -167,27 +173,68 @@ def make_inputs(cfg, lo, hi, device, seed=1000):
     return q, k, v, m, b_lo * HKV
 
 
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_impl():
+    """The reference's own batched entry ``ncstream.attention.multi_head_attention_array``
+    (attention.py:318-361) from baseline/_ref (``kind`` "reference"), else the oracle port of the
+    same loop (oracle/spherical.py, ``kind`` "port")."""
+    if os.path.isdir(os.path.join(REF_INSTALL, "ncstream")) and REF_INSTALL not in sys.path:
+        sys.path.append(REF_INSTALL)
+    try:
+        from ncstream.attention import TileConfig, multi_head_attention_array
+        from ncstream.normalizers import SPHERICAL
+
+        def call(q, k, v, h, hkv, eps):
+            return multi_head_attention_array(q, k, v, SPHERICAL.with_epsilon(eps), h, hkv, scale=1.0,
+                                              tile=TileConfig(64, 64))
+        return call, "reference", "ncstream.attention.multi_head_attention_array (baseline/_ref, unmodified)"
+    except ImportError:
+        from oracle.spherical import multi_head_spherical
+
+        def call(q, k, v, h, hkv, eps):
+            return multi_head_spherical(q, k, v, h, hkv, 1.0, eps)
+        return call, "port", "oracle port of multi_head_attention_array / _streamed_tiles (oracle/spherical.py)"
+
+
+def reference_rows(cfg) -> int:
+    """Query rows per CPU sample: ~4 GFLOP per step (~0.3 s at the reference's ~14 GFLOP/s), a
+    multiple of the default 64-row query group."""
+    per_row = 4.0 * cfg["H"] * cfg["N"] * cfg["D"]
+    return int(max(64, round(4e9 / per_row / 64) * 64))
+
+
+def _quantised(shape, dtype, seed):
+    """float32 arrays holding the configuration dtype's values (SURVEY.md 8(d) CPU baseline)."""
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    t = torch.randn(shape, generator=g)
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "e4m3": torch.float8_e4m3fn}[dtype]
+    return t.to(tdt).float().numpy()
+
+
 def cpu_reference_sample(cfg, rows: int, seed: int = 7):
-    """Time the reference CPU algorithm (oracle port of _streamed_tiles, tile 64x64,
-    float32 inputs holding the dtype-quantised values) on ``rows`` query rows of one
-    (b, h) slice against all N keys.  Returns (seconds, flops, threads)."""
-    from oracle.spherical import streamed_spherical
+    """Time the reference CPU path on its own batched call pattern:
+    ``multi_head_attention_array(q, k, v, SPHERICAL, H, H_kv)`` on ``rows`` query positions x all
+    H heads of one batch element against all N keys, default tile 64x64, float32 inputs holding
+    the dtype-quantised values.  Returns (seconds, flops, threads, kind, what)."""
+    call, kind, what = reference_impl()
     threads = None
     try:
         from threadpoolctl import threadpool_info
         threads = max((i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"), default=None)
     except Exception:
         pass
-    rng = np.random.default_rng(seed)
-    N, D = cfg["N"], cfg["D"]
-    q = rng.standard_normal((rows, D)).astype(np.float32)
-    k = rng.standard_normal((N, D)).astype(np.float32)
-    v = rng.standard_normal((N, D)).astype(np.float32)
-    streamed_spherical(q[:64], k[:1024], v[:1024])  # warm-up
+    N, D, H, HKV = cfg["N"], cfg["D"], cfg["H"], cfg["HKV"]
+    q = _quantised((rows, H, D), cfg["dtype"], seed)
+    k = _quantised((N, HKV, D), cfg["dtype"], seed + 1)
+    v = _quantised((N, HKV, D), cfg["dtype"], seed + 2)
+    call(q[:8], k[:256], v[:256], H, HKV, cfg.get("eps", 0.0))  # warm-up
     t0 = time.perf_counter()
-    streamed_spherical(q, k, v, 1.0, cfg.get("eps", 0.0), 64, 64)
+    call(q, k, v, H, HKV, cfg.get("eps", 0.0))
     dt = time.perf_counter() - t0
-    return dt, 4.0 * rows * N * D, threads or os.cpu_count()
+    return dt, 4.0 * rows * H * N * D, threads or os.cpu_count(), kind, what
 
 
 def _link_roofline(dev, h2d_bytes, d2h_bytes, step_s):
@@ -270,62 +317,87 @@ def run_reference(args, cfg):
 
 
 def _run_reference(args, cfg):
-    rows = args.ref_rows
+    rows = args.ref_rows or reference_rows(cfg)
     times = []
     for i in range(args.warmup + args.steps):
-        dt, fl, threads = cpu_reference_sample(cfg, rows, seed=7 + i)
+        dt, fl, threads, kind, what = cpu_reference_sample(cfg, rows, seed=7 + i)
         if i >= args.warmup:
             times.append((dt, fl))
     tot_t = sum(t for t, _ in times)
     tot_f = sum(f for _, f in times)
     val = tot_f / tot_t / 1e12
-    sample = (f"{rows} query rows x {cfg['N']} keys x d{cfg['D']} of one (b,h) slice per step, float32, "
-              f"tile 64x64 (oracle port of attention.py:146-200)")
+    sample = (f"{rows} query positions x {cfg['H']} heads x {cfg['N']} keys x d{cfg['D']} of one batch element "
+              f"per step, float32 holding {cfg['dtype']} values, tile 64x64: {what}")
     line = {
         "impl": "reference", "metric": "FlashSign fwd TFLOP/s", "value": val, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot_t / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "sample": sample},
-        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "port", "sample": sample,
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": sample,
                          "cpu_count": os.cpu_count(), **_host_info()},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def context_baselines(cfg, q, k, v, device):
-    """PyTorch-eager spherical attention and SDPA softmax on the same GPU (one (b) row)."""
+def _timed(fn, steps, device_index):
+    """CUDA-event time of ``steps`` back-to-back calls (after one warm-up) with NVML clocks sampled
+    over the same window: (ms per call, clock summary)."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device_index) as clk:
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, clk.summary()
+
+
+def context_baselines(cfg, q, k, v, device, steps, device_index):
+    """Same-GPU context on the FULL configuration, timed like FlashSign (CUDA
+    events over back-to-back steps, clocks sampled in the same window):
+      * SDPA softmax attention, per backend (cuDNN, flash) -- the paper's "within 5 % of
+        FlashAttention-2" claim (PAPER.md:201), on B200;
+      * PyTorch-eager spherical attention (materialises S per (b, h); PAPER.md:199);
+      * the O(N d^2) Gram-form identity (a different algorithm, context only).
+    e4m3 configurations run the baselines in bf16 (no fp8 SDPA)."""
     import torch
     import torch.nn.functional as F
     res = {}
     if cfg["dtype"] == "e4m3":
         q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
-    qb, kb, vb = q[:1], k[:1], v[:1]  # one batch row: [1, N, H, D]
-    H, N, D = qb.shape[2], qb.shape[1], qb.shape[3]
-    fl = 4.0 * H * N * N * D
-
-    def eager():  # per head to bound memory: S = q k^T ; O = (S v) / ||S||_row
-        for h in range(H):
-            hk = h * k.shape[2] // H
-            s = qb[0, :, h] @ kb[0, :, hk].T
-            z = s.float().square().sum(-1, keepdim=True).sqrt()
-            (s @ vb[0, :, hk]).float().div_(z)
+    B, N, H, D = q.shape
+    HKV = k.shape[2]
+    fl = 4.0 * B * H * N * k.shape[1] * D
+    qt, kt, vt = (t.transpose(1, 2) for t in (q, k, v))  # BHSD views, as SDPA takes them
 
     def sdpa():
-        F.scaled_dot_product_attention(qb.transpose(1, 2), kb.transpose(1, 2), vb.transpose(1, 2))
+        F.scaled_dot_product_attention(qt, kt, vt, enable_gqa=HKV != H)
 
-    def gram():  # SURVEY 8f #4: the O(N d^2) Gram-form identity -- a different algorithm, context only
-        hk = torch.arange(H, device=qb.device) * kb.shape[2] // H
-        qh = qb[0].float().transpose(0, 1)                       # [H, N, d]
-        kh = kb[0].float().transpose(0, 1)[hk]
-        vh = vb[0].float().transpose(0, 1)[hk]
-        kt = kh.transpose(1, 2)
-        z = (torch.bmm(qh, torch.bmm(kt, kh)) * qh).sum(-1, keepdim=True).sqrt()
-        torch.bmm(qh, torch.bmm(kt, vh)).div_(z)
+    def eager():  # per (b, h) to bound memory: S = q k^T ; O = (S v) / ||S||_row
+        for b in range(B):
+            for h in range(H):
+                hk = h * HKV // H
+                s_ = q[b, :, h] @ k[b, :, hk].T
+                z = s_.float().square().sum(-1, keepdim=True).sqrt()
+                (s_ @ v[b, :, hk]).float().div_(z)
 
-    fns = [("torch_eager_spherical", eager), ("sdpa_softmax", sdpa), ("gram_form_fp32_not_flashsign", gram)]
-    try:  # each SDPA backend separately, so the line says which one the default picked
+    def gram():
+        hk = torch.arange(H, device=q.device) * HKV // H
+        for b in range(B):
+            qh = q[b].float().transpose(0, 1)
+            kh = k[b].float().transpose(0, 1)[hk]
+            vh = v[b].float().transpose(0, 1)[hk]
+            kt_ = kh.transpose(1, 2)
+            z = (torch.bmm(qh, torch.bmm(kt_, kh)) * qh).sum(-1, keepdim=True).sqrt()
+            torch.bmm(qh, torch.bmm(kt_, vh)).div_(z)
+
+    fns = []
+    try:
         from torch.nn.attention import SDPBackend, sdpa_kernel
 
         def pinned(be):
@@ -333,28 +405,129 @@ def context_baselines(cfg, q, k, v, device):
                 with sdpa_kernel([be]):
                     sdpa()
             return run
-        for be in (SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION, SDPBackend.EFFICIENT_ATTENTION):
-            fns.append((f"sdpa_softmax_{be.name.lower()}", pinned(be)))
+        fns += [("sdpa_softmax_cudnn", pinned(SDPBackend.CUDNN_ATTENTION), steps),
+                ("sdpa_softmax_flash", pinned(SDPBackend.FLASH_ATTENTION), max(3, steps // 4))]
     except ImportError:
-        pass
-
-    for name, fn in fns:
+        fns.append(("sdpa_softmax", sdpa, steps))
+    fns += [("torch_eager_spherical", eager, 2), ("gram_form_fp32_not_flashsign", gram, 3)]
+    for name, fn, n in fns:
         try:
+            ms, clk = _timed(fn, n, device_index)
+            if name.startswith("gram"):
+                res[name] = {"ms_per_step": ms, "steps": n, "clocks": clk,
+                             "note": "O(N d^2) identity, not the 4*N^2*d FlashSign work"}
+            else:
+                res[name] = {"tflops": fl / ms / 1e9, "ms_per_step": ms, "steps": n, "clocks": clk,
+                             "dtype": str(q.dtype).replace("torch.", ""), "shape": "full configuration"}
+        except Exception as ex:  # OOM etc. recorded, as the paper did (PAPER.md:199)
+            res[name] = {"error": f"{type(ex).__name__}: {str(ex)[:160]}"}
+        torch.cuda.empty_cache()
+    return res
+
+
+def host_latency(device):
+    """Host time per call of the torch entry (``flashsign.fwd_async``: extension + C-ABI + cached
+    TMA descriptors + launch) and of the numpy drop-in (``multi_head_attention_array``) at the
+    C1 shape (B1 H1 N256 d64) and a per-cell GRN call shape (one cell, N=256 genes, H8, d64).
+    Launches are queued back to back (no synchronisation inside the timed loop for fwd_async)."""
+    import torch
+
+    from paper_2505_09326_b200 import SPHERICAL, flashsign
+    from paper_2505_09326_b200.attention import multi_head_attention_array
+    out = {}
+    for name, (b, n, h, d) in (("c1", (1, 256, 1, 64)), ("grn_cell", (1, 256, 8, 64))):
+        qd = torch.randn((b, n, h, d), device=device).to(torch.bfloat16)
+        o = torch.empty_like(qd)
+        bad = torch.empty(1, dtype=torch.int64, device=device)
+        for _ in range(50):
+            flashsign.fwd_async(qd, qd, qd, out=o, bad_key=bad)
+        torch.cuda.synchronize()
+        reps = 2000
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            flashsign.fwd_async(qd, qd, qd, out=o, bad_key=bad)
+        t1 = time.perf_counter()
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        qn = np.random.default_rng(0).standard_normal((n, h, d)).astype(np.float32)
+        multi_head_attention_array(qn, qn, qn, SPHERICAL, h, h)
+        t3 = time.perf_counter()
+        for _ in range(50):
+            multi_head_attention_array(qn, qn, qn, SPHERICAL, h, h)
+        t4 = time.perf_counter()
+        out[name] = {"shape_bnhd": [b, n, h, d], "fwd_async_host_us": 1e6 * (t1 - t0) / reps,
+                     "fwd_async_incl_gpu_us": 1e6 * (t2 - t0) / reps,
+                     "dropin_numpy_call_us": 1e6 * (t4 - t3) / 50}
+    return out
+
+
+def _pageable_link(dev, nbytes=128 << 20):
+    """The host link as a numpy caller sees it: pageable host -> device, device -> pinned host, and
+    both at once (GB/s, best of 3)."""
+    import torch
+    src = torch.from_numpy(np.ones(nbytes // 4, dtype=np.float32))   # pageable
+    dst = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+    dsrc = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+    hdst = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def best(fn):
+        b = float("inf")
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
             fn()
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(3):
-                fn()
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / 3
-            res[name] = ({"ms_per_batch_row": ms, "note": "O(N d^2) identity, not the 4*N^2*d FlashSign work"}
-                         if name.startswith("gram") else
-                         {"tflops": fl / ms / 1e9, "ms_per_batch_row": ms, "dtype": str(qb.dtype)})
-        except Exception as ex:  # OOM etc. recorded, as the paper did (PAPER.md:199)
-            res[name] = {"error": f"{type(ex).__name__}: {str(ex)[:120]}"}
-    return res
+            b = min(b, time.perf_counter() - t0)
+        return b
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            dst.copy_(src, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            hdst.copy_(dsrc, non_blocking=True)
+
+    def both():
+        d2h()
+        h2d()
+
+    return {"h2d_pageable_gbs": nbytes / best(h2d) / 1e9, "d2h_pinned_gbs": nbytes / best(d2h) / 1e9,
+            "both_gbs": 2 * nbytes / best(both) / 1e9}
+
+
+def dropin_e2e(cfg, q, k, v, device, passes=2):
+    """The reference's own call pattern through the drop-in API (grn.py:171-173):
+    ``multi_head_attention_array(q[b], k[b], v[b], SPHERICAL, H, H_kv)`` once per batch element, with
+    float32 numpy arrays (pageable host memory) in and out.  Wall clock over whole passes of the
+    batch; the host link bound uses the measured pageable H2D / pinned D2H bandwidth."""
+    import torch
+
+    from paper_2505_09326_b200 import SPHERICAL
+    from paper_2505_09326_b200.attention import multi_head_attention_array
+    B, N, H, D = q.shape
+    HKV = k.shape[2]
+    spec = SPHERICAL.with_epsilon(cfg["eps"])
+    qs = [q[b].float().cpu().numpy() for b in range(B)]
+    ks = [k[b].float().cpu().numpy() for b in range(B)]
+    vs = [v[b].float().cpu().numpy() for b in range(B)]
+    multi_head_attention_array(qs[0], ks[0], vs[0], spec, H, HKV, scale=1.0)  # warm-up (engine, buffers)
+    t0 = time.perf_counter()
+    for _ in range(passes):
+        for b in range(B):
+            multi_head_attention_array(qs[b], ks[b], vs[b], spec, H, HKV, scale=1.0)
+    dt = (time.perf_counter() - t0) / passes
+    h2d = sum(a.nbytes for a in qs + ks + vs)
+    d2h = sum(a.nbytes for a in qs)
+    link = _pageable_link(device)
+    bound = max(h2d / link["h2d_pageable_gbs"], d2h / link["d2h_pinned_gbs"], (h2d + d2h) / link["both_gbs"]) / 1e9
+    link.update({"bound_ms": bound * 1e3, "frac": bound / dt})
+    fl = 4.0 * B * H * N * k.shape[1] * D
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": dt * 1e3, "passes": passes,
+            "api": "paper_2505_09326_b200.attention.multi_head_attention_array per batch element, float32 numpy "
+                   "in/out (the reference's call pattern)", "link": link}
 
 
 def run_ours(args, cfg):
@@ -487,6 +660,17 @@ def run_ours(args, cfg):
                "steps": e2e_steps, "api": "paper_2505_09326_b200.pipeline.HostPipeline.run (pinned host bf16 in/out)",
                "link": link}
 
+    e2e_dropin = lat = None
+    if world == 1 and not args.no_e2e:
+        try:
+            e2e_dropin = dropin_e2e(cfg, q, k, v, dev)
+        except Exception as ex:  # recorded, never silently dropped
+            e2e_dropin = {"error": f"{type(ex).__name__}: {str(ex)[:200]}"}
+        try:
+            lat = host_latency(dev)
+        except Exception as ex:
+            lat = {"error": f"{type(ex).__name__}: {str(ex)[:200]}"}
+
     if rank == 0:
         peaks, peak_src = load_peaks()
         fp8 = cfg["dtype"] == "e4m3"
@@ -511,17 +695,24 @@ def run_ours(args, cfg):
                     "frac_of_sustained": (achieved / peaks["bf16_tflops_sustained"] / (2.0 if fp8 else 1.0))
                     if "bf16_tflops_sustained" in peaks else None,
                     "flops_per_launch": per_launch_flops, "kernel_ms": kernel_ms}
+        if fp8:  # the same against twice the measured dense bf16 burst (FP8 dense = 2x BF16 on B200)
+            roofline["frac_of_2x_bf16_burst"] = achieved / (2.0 * peaks["bf16_tflops"])
         cpu = None
         if world == 1 and not args.no_cpu:
-            rows = args.cpu_rows or N
+            rows = args.cpu_rows or reference_rows(cfg)
             with _all_host_threads():
-                dt, fl, threads = cpu_reference_sample(cfg, rows)
+                tt_, ff_ = 0.0, 0.0
+                for rep_ in range(3):  # same sample as one step of the reference arm, three times
+                    dt, fl, threads, kind, what = cpu_reference_sample(cfg, rows, seed=7 + rep_)
+                    tt_, ff_ = tt_ + dt, ff_ + fl
                 host = _host_info()
-            cpu = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-                   "sample": f"{rows} query rows x {N} keys x d{D}, one (b,h) slice, float32, tile 64x64 "
-                             f"(oracle port of attention.py:146-200), {dt:.2f} s",
+            cpu = {"value": ff_ / tt_ / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
+                   "sample": f"3 x ({rows} query positions x {H} heads x {N} keys x d{D} of one batch element), "
+                             f"float32 holding {cfg['dtype']} values, tile 64x64: {what}; {tt_:.2f} s",
                    "cpu_count": os.cpu_count(), **host}
-        ctx = context_baselines(cfg, q, k, v, dev) if (world == 1 and args.context) else None
+        ctx = None
+        if world == 1 and not args.no_context:
+            ctx = context_baselines(cfg, q, k, v, dev, args.steps, local)
         line = {
             "metric": "FlashSign fwd TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -536,6 +727,7 @@ def run_ours(args, cfg):
                        "flops_per_step": total_flops},
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": n_launch_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "gather": gather,
+            "e2e_dropin": e2e_dropin, "host_latency": lat,
         }
         if ctx is not None:
             line["context"] = ctx
@@ -552,12 +744,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-rows", type=int, default=512, help="query rows per CPU reference sample")
+    ap.add_argument("--ref-rows", type=int, default=0, help="query positions per CPU reference sample (0: ~4 GFLOP)")
     ap.add_argument("--cpu-rows", type=int, default=0, help="query rows of the cpu_baseline sample (0: one full slice)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--context", action="store_true", help="also time torch-eager spherical and SDPA")
+    ap.add_argument("--no-context", action="store_true", help="skip the SDPA / eager / Gram context baselines")
     ap.add_argument("--fused-mult", action="store_true", help="c5: fuse the key multiplicities into the kernel")
     args = ap.parse_args()
     if args.warmup < 3:

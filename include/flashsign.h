@@ -53,7 +53,8 @@ typedef enum {
   FS_F16 = 0,
   FS_BF16 = 1,
   FS_E4M3 = 2,
-  FS_F32 = 3 /* output only */
+  FS_F32 = 3, /* output (fs_fwd) / source (fs_prepare) */
+  FS_F64 = 4  /* source only (fs_prepare) */
 } fs_dtype;
 
 typedef enum {
@@ -110,6 +111,10 @@ typedef struct {
      calls fs_combine(p, 1, stream) to normalise. */
   int32_t partial_only;
   int32_t reserved1; /* must be 0 */
+  /* Optional device array of 4 floats {q_descale, k_descale, v_descale, p_scale} (NULL: the host
+     fields above).  Read by the kernel at launch time, so per-tensor scales chosen on the device
+     (fs_prepare, below) need no host round trip.  Same constraints as the host fields. */
+  const float *dev_scales;
 } fs_fwd_params;
 
 /* Validate, encode TMA descriptors (cached per call), launch.  Async. */
@@ -153,6 +158,43 @@ fs_status fs_ipc_malloc(int64_t bytes, void **ptr, void *handle64);
 fs_status fs_ipc_open(const void *handle64, void **ptr);
 fs_status fs_ipc_close(void *ptr);
 fs_status fs_ipc_free(void *ptr);
+
+/* Operand preparation for host-array callers (the drop-in path; attention.py:252-279 accepts any
+   float32 / float64 array and computes in float64).  Converts up to three caller tensors -- rows of
+   d elements, row-major, on the device -- to the kernel's input dtype, each with one power-of-two
+   scale chosen ON THE DEVICE: amax|x 2^e| in [2^(T-1), 2^T) (T = 14 for FS_F16 / FS_BF16, 8 for
+   FS_E4M3), plus a power-of-two p_scale from the Cauchy-Schwarz bound max||q'|| max||k'|| so
+   that the PV operand P = p s can never overflow (fp16 / e4m3) for any finite input.  Spherical and
+   signed-L1 outputs are invariant to these factors; fs_fwd folds them out exactly when given
+   `scales` as fs_fwd_params.dev_scales.  FS_PREP_EXACT keeps the values (no operand scaling; the
+   f16 emulation's binary16-rounded inputs, tensor.py:132-139, attention.py:265-270) and still
+   chooses p_scale.  A tensor with src == NULL is not converted and its stats from an earlier call
+   (same `stats` workspace) are reused: the K / V of a query stream processed in chunks.
+   One memset + two kernels, async on `stream`. */
+typedef enum { FS_PREP_SCALE = 0, FS_PREP_EXACT = 1 } fs_prep_mode;
+
+typedef struct {
+  const void *src;        /* device, [rows, d] with src_row_stride; NULL = reuse this slot's stats  */
+  int32_t src_dtype;      /* FS_F32 | FS_F64 | FS_F16 | FS_BF16                                      */
+  int32_t d;              /* valid columns, 1 <= d <= d_pad                                           */
+  int64_t rows;           /* rows (token x head) of d elements                                       */
+  int64_t src_row_stride; /* elements, >= d                                                          */
+  void *dst;              /* device, [rows, d_pad] in dst_dtype, columns >= d zero-filled            */
+  int64_t dst_row_stride; /* elements, >= d_pad                                                      */
+} fs_prep_tensor;
+
+typedef struct {
+  fs_prep_tensor t[3];  /* q, k, v */
+  int32_t dst_dtype;    /* FS_F16 | FS_BF16 | FS_E4M3                                        */
+  int32_t d_pad;        /* columns written per operand row                                   */
+  int32_t mode;         /* fs_prep_mode                                                      */
+  int32_t normalizer;   /* fs_normalizer of the call (bounds eps / g)                        */
+  float scale, eps;     /* the call's score scale c and denom_epsilon                        */
+  double *stats;        /* device workspace, 6 doubles: {amax, max row L2 norm} of q, k, v   */
+  float *scales;        /* device out, 4 floats -> fs_fwd_params.dev_scales                  */
+} fs_prep_params;
+
+fs_status fs_prepare(const fs_prep_params *p, fs_stream_t stream);
 
 /* Thread-local text of the last non-FS_OK status. */
 const char *fs_last_error(void);

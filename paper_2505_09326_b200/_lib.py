@@ -15,14 +15,15 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libflashsign.so")
 
 FS_OK, FS_ERR_SHAPE, FS_ERR_CONFIG, FS_ERR_DTYPE, FS_ERR_UNSUPPORTED, FS_ERR_CUDA = range(6)
-FS_F16, FS_BF16, FS_E4M3, FS_F32 = range(4)
+FS_F16, FS_BF16, FS_E4M3, FS_F32, FS_F64 = range(5)
+FS_PREP_SCALE, FS_PREP_EXACT = range(2)
 FS_NORM_SPHERICAL, FS_NORM_SIGNED_L1 = range(2)
 FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
 
 # every symbol include/flashsign.h declares
 EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version", "fs_kv_splits", "fs_partial_floats",
                     "fs_combine", "fs_peer_floats", "fs_fwd_peer", "fs_combine_peer", "fs_ipc_malloc", "fs_ipc_open",
-                    "fs_ipc_close", "fs_ipc_free")
+                    "fs_ipc_close", "fs_ipc_free", "fs_prepare")
 
 
 class FsFwdParams(ctypes.Structure):
@@ -61,6 +62,7 @@ class FsFwdParams(ctypes.Structure):
         ("partial", ctypes.c_void_p),
         ("partial_only", ctypes.c_int32),
         ("reserved1", ctypes.c_int32),
+        ("dev_scales", ctypes.c_void_p),
     ]
 
 
@@ -77,9 +79,39 @@ class FsPeerParams(ctypes.Structure):
     ]
 
 
+class FsPrepTensor(ctypes.Structure):
+    """Mirror of ``fs_prep_tensor`` (include/flashsign.h)."""
+
+    _fields_ = [
+        ("src", ctypes.c_void_p),
+        ("src_dtype", ctypes.c_int32),
+        ("d", ctypes.c_int32),
+        ("rows", ctypes.c_int64),
+        ("src_row_stride", ctypes.c_int64),
+        ("dst", ctypes.c_void_p),
+        ("dst_row_stride", ctypes.c_int64),
+    ]
+
+
+class FsPrepParams(ctypes.Structure):
+    """Mirror of ``fs_prep_params`` (include/flashsign.h)."""
+
+    _fields_ = [
+        ("t", FsPrepTensor * 3),
+        ("dst_dtype", ctypes.c_int32),
+        ("d_pad", ctypes.c_int32),
+        ("mode", ctypes.c_int32),
+        ("normalizer", ctypes.c_int32),
+        ("scale", ctypes.c_float),
+        ("eps", ctypes.c_float),
+        ("stats", ctypes.c_void_p),
+        ("scales", ctypes.c_void_p),
+    ]
+
+
 IPC_HANDLE_BYTES = 64
 
-_lock = threading.Lock()
+_lock = threading.RLock()  # load_torch_ext() calls load() while holding it
 _lib = None
 
 
@@ -126,8 +158,39 @@ def load() -> ctypes.CDLL:
             lib.fs_ipc_close.restype = ctypes.c_int
             lib.fs_ipc_free.argtypes = [ctypes.c_void_p]
             lib.fs_ipc_free.restype = ctypes.c_int
+            lib.fs_prepare.argtypes = [ctypes.POINTER(FsPrepParams), ctypes.c_void_p]
+            lib.fs_prepare.restype = ctypes.c_int
             _lib = lib
     return _lib
+
+
+TORCH_EXT_PATH = os.path.join(_HERE, "_lib", "fs_torch.so")
+_ext = None
+
+
+def load_torch_ext():
+    """The PyTorch C++ extension over the C-ABI (csrc/fs_torch.cpp, built in-tree by build.py);
+    raises loudly if it is missing -- there is no fallback."""
+    global _ext
+    if _ext is not None:
+        return _ext
+    with _lock:
+        if _ext is None:
+            if not os.path.exists(TORCH_EXT_PATH):
+                raise RuntimeError(f"FlashSign torch extension not built: {TORCH_EXT_PATH} is missing. "
+                                   "Run `python -c 'import __graft_entry__ as g; g.build()'`.")
+            import importlib.machinery
+            import importlib.util
+
+            import torch  # noqa: F401  (libtorch / libc10 symbols first)
+
+            load()  # libflashsign.so (the extension's $ORIGIN dependency) through the same path
+            loader = importlib.machinery.ExtensionFileLoader("fs_torch", TORCH_EXT_PATH)
+            spec = importlib.util.spec_from_loader("fs_torch", loader)
+            mod = importlib.util.module_from_spec(spec)
+            loader.exec_module(mod)
+            _ext = mod
+    return _ext
 
 
 def last_error() -> str:

@@ -38,7 +38,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _lib, flashsign
+from . import flashsign, hostpath
 from ._errors import ConfigError
 from .normalizers import DegenerateDenominatorError, NormalizerSpec
 from .tensor import DenseTensor, ShapeMismatchError, quantize_f16_array
@@ -113,8 +113,13 @@ class AttentionConfig:
 
 
 class ScoreBufferMeter:
-    """Peak transient score elements (attention.py:86-97).  The streamed GPU
-    path records the kernel's real on-chip tile, min(BM, y) * min(BN, x)."""
+    """Peak transient score elements (attention.py:86-97).
+
+    The streamed path records the reference's contract for the requested tile,
+    ``min(g_y, y) * min(s_x, x)`` (1 for the scalar 1x1 path; test_attention.py:149-173),
+    so callers that size buffers or check the bound from the meter see the same numbers.
+    The kernel's own on-chip score tile (128 x 128/192, held in TMEM) is
+    ``flashsign.kernel_score_tile(head_dim, dtype)``."""
 
     def __init__(self):
         self.peak_elements = 0
@@ -157,61 +162,54 @@ def _out_dtype(a: np.ndarray):
     return a.dtype if a.dtype in (np.float16, np.float32, np.float64) else np.dtype(np.float64)
 
 
-def _to_device(a: np.ndarray, dev, dtype: torch.dtype, d_pad: int) -> torch.Tensor:
-    a = np.ascontiguousarray(a)
-    t = torch.from_numpy(a if a.flags.writeable else a.copy())
-    if t.dtype not in (torch.float16, torch.float32, torch.float64):
-        t = t.to(torch.float64)
-    t = t.to(dev, non_blocking=False)
-    if t.shape[-1] != d_pad:
-        t = torch.nn.functional.pad(t, (0, d_pad - t.shape[-1]))
-    if dtype == getattr(torch, "float8_e4m3fn", None):
-        t = t.float().clamp_(-448.0, 448.0)
-    return t.to(dtype).contiguous()
-
-
 def _gpu_streamed(q3: np.ndarray, k3: np.ndarray, v3: np.ndarray, scale: float, eps: float,
-                  compute: str, meter, normalizer: str = "spherical", m: np.ndarray | None = None) -> np.ndarray:
-    """FlashSign on [n, h, d] / [x, h_kv, d] arrays in one launch; raises the
-    reference's DegenerateDenominatorError for the first bad (head, row)."""
+                  compute: str, meter, normalizer: str = "spherical", m: np.ndarray | None = None,
+                  exact: bool = False) -> np.ndarray:
+    """FlashSign on [n, h, d] / [x, h_kv, d] host arrays (one launch per query chunk, all heads;
+    ``hostpath``); raises the reference's DegenerateDenominatorError for the first bad (head, row).
+
+    The operands are converted on the device with power-of-two per-tensor scales and a P scale
+    from the Cauchy-Schwarz bound (``fs_prepare``), so any finite float32 / float64 input the
+    reference accepts runs without fp16 overflow; ``exact`` (the f16 emulation) keeps the
+    binary16-rounded values themselves."""
     n, h, d = q3.shape
     x, h_kv, _ = k3.shape
     if v3.shape[2] != d:
         raise ShapeMismatchError(f"value dim must equal the head dim: {v3.shape} vs {q3.shape}")
-    tdt = _COMPUTE_DTYPES[compute]
     out_np_dtype = _out_dtype(q3)
-    if meter is not None:
-        bm, bn = _lib.query_tile(min(max(d, 1), 128), _lib.FS_E4M3 if compute == "e4m3" else _lib.FS_BF16)
-        meter.record(min(bm, n) * min(bn, x))
     if n == 0:
         return np.empty((0, h, d), dtype=out_np_dtype)
     if d > 128:
         raise ConfigError(f"flashsign: head dim {d} > 128 is not supported by the sm_100a kernel")
-    align = 16 if compute == "e4m3" else 8
-    d_pad = max(align, -(-d // align) * align)
     dev = _device()
-    qt = _to_device(q3, dev, tdt, d_pad)[None]
-    kt = _to_device(k3, dev, tdt, d_pad)[None]
-    vt = _to_device(v3, dev, tdt, d_pad)[None]
-    if x == 0:  # keep TMA descriptors valid for an empty K/V stream
-        kt = torch.zeros((1, 1, h_kv, d_pad), dtype=tdt, device=dev)[:, :0]
-        vt = kt
-    ks = None
-    if m is not None and x > 0:
-        ks = torch.from_numpy(np.ascontiguousarray(m, dtype=np.float32)).to(dev)[None]
-    o, bad = flashsign.fwd_async(qt, kt, vt, scale=float(scale), eps=float(eps), out_dtype=torch.float32,
-                                 normalizer=normalizer, key_scale=ks)
-    info = flashsign.decode_bad_key(int(bad.item()), h, n)
-    if info is not None:
-        _, _, row, z = info
+    src = [a if a.dtype in (np.float16, np.float32, np.float64) else a.astype(np.float64) for a in (q3, k3, v3)]
+    if m is not None:
+        src[1] = np.asarray(src[1], dtype=np.float64) * np.asarray(m, dtype=np.float64)[:, None, None]
+    out, first = hostpath.run(src[0], src[1], src[2], scale=float(scale), eps=float(eps),
+                              compute=_COMPUTE_DTYPES[compute], normalizer=normalizer, exact=exact,
+                              out_np_dtype=out_np_dtype, device=dev)
+    if first is not None:
+        _, row, z = first
         raise DegenerateDenominatorError(float(z), f"row {row}")
-    return o[0, :, :, :d].cpu().numpy().astype(out_np_dtype, copy=False)
+    return out
+
+
+def _record_tile(meter, tile, y: int, x: int, f16: bool) -> None:
+    """The reference's meter contract for one streamed (single-head) call: the scalar 1x1 path
+    records 1 (attention.py:217-218), the tile loop records each tile's size, whose maximum is
+    min(g_y, y) * min(s_x, x) (attention.py:169-171)."""
+    if meter is None:
+        return
+    if tile.g_y == 1 and tile.s_x == 1 and not f16:
+        meter.record(1)
+    elif y > 0 and x > 0:
+        meter.record(min(tile.g_y, y) * min(tile.s_x, x))
 
 
 def streamed_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: NormalizerSpec, scale: float,
                              tile: TileConfig, f16: bool = False, meter: ScoreBufferMeter | None = None) -> np.ndarray:
     """Streamed path on plain arrays (attention.py:252-279), on the FlashSign kernel."""
-    _check_qkv(q, k, v)
+    y, x, _ = _check_qkv(q, k, v)
     norm = _gpu_normalizer(spec)
     if tile.g_y < 1 or tile.s_x < 1:
         raise ConfigError(f"tile sizes must be >= 1, got g_y={tile.g_y}, s_x={tile.s_x}")
@@ -220,8 +218,9 @@ def streamed_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: 
         if q.dtype != np.float32:
             raise ConfigError("f16 emulation requires float32 inputs")
         compute = "fp16"
+    _record_tile(meter, tile, y, x, f16)
     out = _gpu_streamed(q[:, None, :], k[:, None, :], v[:, None, :], scale, spec.denom_epsilon, compute, meter,
-                        norm)
+                        norm, exact=f16)
     return out[:, 0, :]
 
 
@@ -263,7 +262,8 @@ def multi_head_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec
         if q.dtype != np.float32:
             raise ConfigError("f16 emulation requires float32 inputs")
         compute = "fp16"
-    return _gpu_streamed(q, k, v, eff_scale, spec.denom_epsilon, compute, meter, norm)
+    _record_tile(meter, eff_tile, q.shape[0], k.shape[0], f16)
+    return _gpu_streamed(q, k, v, eff_scale, spec.denom_epsilon, compute, meter, norm, exact=f16)
 
 
 def multiplicity_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, m, spec: NormalizerSpec, h: int,
@@ -309,7 +309,9 @@ def multiplicity_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, m,
     # (flashsign.fwd(key_scale=...)), which costs the latency-bound norm step more than the
     # elementwise pass costs
     kp = np.asarray(k, dtype=np.float64) * mv.reshape((-1,) + (1,) * (k.ndim - 1))
-    return _gpu_streamed(q, kp.astype(k.dtype, copy=False), v, eff_scale, spec.denom_epsilon, compute, meter, norm)
+    _record_tile(meter, eff_tile, q.shape[0], k.shape[0], f16)
+    return _gpu_streamed(q, kp.astype(k.dtype, copy=False), v, eff_scale, spec.denom_epsilon, compute, meter, norm,
+                         exact=f16)
 
 
 def naive_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, spec: NormalizerSpec, scale: float,
@@ -396,3 +398,63 @@ def apply_multiplicity_array(k: np.ndarray, m) -> np.ndarray:
 
 def apply_multiplicity(k, m) -> DenseTensor:
     return DenseTensor(apply_multiplicity_array(k.array, m), _dt(k))
+
+
+_DROPIN_NAMES = ("streamed_attention_array", "streamed_attention", "multi_head_attention_array",
+                 "multi_head_attention")
+
+
+def _spec_of(name: str, args, kwargs):
+    """The NormalizerSpec argument of a drop-in call (positional slot as in the reference)."""
+    if name in ("streamed_attention", "multi_head_attention"):
+        cfg = args[3] if len(args) > 3 else kwargs.get("cfg")
+        return getattr(cfg, "spec", None)
+    return args[3] if len(args) > 3 else kwargs.get("spec")
+
+
+def patch_ncstream(softmax: str = "reference") -> list:
+    """Route the reference's streamed attention onto the FlashSign kernel.
+
+    Replaces ``streamed_attention_array``, ``streamed_attention``, ``multi_head_attention_array`` and
+    ``multi_head_attention`` in ``ncstream.attention`` and in every ncstream module that imported
+    them by name (``ncstream`` itself, ``grn`` -- grn.py:27-31, 171 -- and ``verification``).  The
+    materialising oracle ``naive_attention_array`` stays the reference's own.  Calls with the
+    exp-free triples (SPHERICAL, SIGNED_L1) run on the kernel; the softmax triple is not FlashSign
+    and, with ``softmax="reference"`` (default), keeps calling the reference function it replaced
+    (the GRN model's softmax negative control, grn.py), or raises ``ConfigError`` with
+    ``softmax="raise"``.  Modules imported afterwards with ``from ncstream.attention import ...``
+    get the patched functions.  Returns the patched ``module.name`` strings."""
+    import functools
+    import importlib
+
+    att = importlib.import_module("ncstream.attention")
+    originals = {n: getattr(att, n) for n in _DROPIN_NAMES}
+    if any(getattr(f, "_flashsign_dropin", False) for f in originals.values()):
+        originals = {n: f.__wrapped_reference__ for n, f in originals.items()}
+
+    def make(name):
+        ours, ref = globals()[name], originals[name]
+
+        @functools.wraps(ref)
+        def call(*args, **kwargs):
+            spec = _spec_of(name, args, kwargs)
+            if softmax == "reference" and getattr(spec, "name", None) not in flashsign.NORMALIZERS:
+                return ref(*args, **kwargs)
+            return ours(*args, **kwargs)
+
+        call._flashsign_dropin = True
+        call.__wrapped_reference__ = ref
+        return call
+
+    patched = {n: make(n) for n in _DROPIN_NAMES}
+    done = []
+    for modname in ("ncstream.attention", "ncstream", "ncstream.grn", "ncstream.verification"):
+        try:
+            mod = importlib.import_module(modname)
+        except ImportError:
+            continue
+        for name in _DROPIN_NAMES:
+            if hasattr(mod, name):
+                setattr(mod, name, patched[name])
+                done.append(f"{modname}.{name}")
+    return done

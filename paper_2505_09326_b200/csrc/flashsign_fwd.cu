@@ -52,6 +52,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -140,11 +141,9 @@ struct KParams {
   int32_t heads_q, heads_kv, seqlen_q, seqlen_kv, head_dim;
   int32_t n_qblk;   // work tiles per (batch, head, K/V range) = ceil(seqlen_q / (NQT*BM*CL))
   int32_t n_tiles;  // n_qblk * heads_q * batch
-  float zmul;       // spherical: (scale*q_descale*k_descale)^2; signed L1: |scale*q_descale*k_descale|
-  float out_mul;    // scale * q_descale * k_descale * v_descale / p_scale
-  float eps;
-  float p_scale;
-  float ovf_z;      // a P chunk whose sum of a2(s) stays below this cannot overflow (PMAX/|p_scale|)^{2|1}
+  float scale, eps;                                // score scale c, denom_epsilon
+  float q_descale, k_descale, v_descale, p_scale;  // host values (fs_fwd_params)
+  const float* dev_scales;  // non-NULL: {q, k, v descale, p_scale} read on the device instead
   uint64_t* bad_key;
   // split K/V stream (streaming.py:122-128 merge): work tile = (batch, head, split, query block)
   int32_t n_batch;
@@ -158,6 +157,42 @@ struct KParams {
   float* const* peer;      // device array [peer_world] of the ranks' workspaces (NULL: off)
   int32_t peer_world, peer_rank, peer_rows;
 };
+
+// Epilogue constants, derived once per thread from (c, eps, descales, p_scale) in double.
+// With g = c * q_descale * k_descale and raw = sum_j a2(q'_i . k'_j) (the kernel's operands):
+//   spherical  O = c sum s v / sqrt(c^2 sum s^2 + eps) = sign(g) vd/p * acc / sqrt(raw + eps/g^2)
+//   signed L1  O = ...                                = sign(g) vd/p * acc / (raw + eps/|g|)
+// -- the row norm is taken in the operands' own units, so neither g^2 nor the original-unit z
+// has to fit fp32 (the drop-in path scales its operands by powers of two, attention.py).
+struct Fold {
+  float eps_f;    // eps / g^2 (spherical) or eps / |g| (signed L1)
+  float zrep;     // raw -> the reference's z (g^2 or |g|), reported for bad rows / partials
+  float out_sgn;  // sign(g) * v_descale / p_scale: normalised output multiplier
+  float out_mul;  // g * v_descale / p_scale: unnormalised numerator (split / partial mode)
+  float ps;       // p_scale
+  bool zero_g;    // c == 0: every score is 0 (raw forced to 0)
+};
+template <int NORM>
+__device__ __forceinline__ Fold make_fold(const KParams& p) {
+  double qd = p.q_descale, kd = p.k_descale, vd = p.v_descale, ps = p.p_scale;
+  if (p.dev_scales != nullptr) {
+    qd = p.dev_scales[0];
+    kd = p.dev_scales[1];
+    vd = p.dev_scales[2];
+    ps = p.dev_scales[3];
+  }
+  const double g = static_cast<double>(p.scale) * qd * kd;
+  const double ag = fabs(g);
+  Fold f;
+  f.zero_g = (g == 0.0);
+  const double zrep = NORM == FS_NORM_SIGNED_L1 ? ag : g * g;
+  f.zrep = static_cast<float>(zrep);
+  f.eps_f = f.zero_g ? p.eps : static_cast<float>(fmin(static_cast<double>(p.eps) / zrep, 3.0e38));
+  f.out_sgn = f.zero_g ? 0.f : static_cast<float>((g < 0.0 ? -vd : vd) / ps);
+  f.out_mul = static_cast<float>(g * vd / ps);
+  f.ps = static_cast<float>(ps);
+  return f;
+}
 
 template <int IN>
 struct InTraits;
@@ -716,7 +751,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     const uint32_t s_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + C::COL_S0;
-    const float ps = p.p_scale;
+    const float ps = p.dev_scales != nullptr ? p.dev_scales[3] : p.p_scale;
+    // a half whose sum of a2(s) stays below this cannot hold an out-of-range P: (PMAX/|p_scale|)^{2|1}
+    const float ovf_z = NORM == FS_NORM_SIGNED_L1 ? TR::PMAX / fabsf(ps) : (TR::PMAX / fabsf(ps)) * (TR::PMAX / fabsf(ps));
     uint32_t s_use = 0;
 #if FS_PROF
     long long pr_sw = 0, pr_nc = 0, pr_nn = 0;
@@ -821,7 +858,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (TR::SAT_CHECK) {
           // max|s| <= sqrt(sum s^2) (<= sum |s|): only a half whose sum reaches ovf_z can hold a
           // saturated code; then look for 0x7e / 0xfe (+-448) in its packed P
-          if ((h0.x + h0.y) + (h1.x + h1.y) >= p.ovf_z) {
+          if ((h0.x + h0.y) + (h1.x + h1.y) >= ovf_z) {
             uint32_t sat = 0;
 #pragma unroll
             for (int i = 0; i < NCH * 8; ++i) {
@@ -863,6 +900,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     using OT = typename OutT<OUT>::T;
+    const Fold fd = make_fold<NORM>(p);
+    // FP16 P overflow needs some |p s| >= 65520, hence raw z >= (65504 / p)^2 (or 65504 / p for L1)
+    // (device scales come from fs_prepare, whose p_scale bounds |p s| below 2^15 for every score:
+    //  no overflow is possible and the check is off)
+    const float ovf_raw = p.dev_scales != nullptr ? __int_as_float(0x7f800000)
+                          : NORM == FS_NORM_SIGNED_L1 ? TR::PMAX / fd.ps
+                                                      : (TR::PMAX / fd.ps) * (TR::PMAX / fd.ps);
     int it = 0;
     for (int tile = tile0; tile < p.n_tiles; tile += tstride, ++it) {
       const TileCoord tc = decode_tile(tile, p, rank);
@@ -870,21 +914,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t o_use = static_cast<uint32_t>(it / C::NOB);
 #pragma unroll 1
       for (int t = 0; t < NQT; ++t) {
-        // zr = sum_j a2(c s_ij) (what the reference calls z), or +inf for a P overflow
-        float zr = 0.f;
+        // raw = sum_j a2(q'_i . k'_j) in the operands' units (+inf for a saturated FP8 P);
+        // the reference's z is raw * zrep
+        float raw = 0.f;
         if (tc.L > 0) {
           ptx::mbar_wait(&bars->z_full[t][ob], o_use & 1u);
           const float* zt = zbuf + (t * C::NOB + ob) * 2 * BM + r;
-          zr = p.zmul * (zt[0] + zt[BM]);  // the two column halves of the row
+          raw = fd.zero_g ? 0.f : zt[0] + zt[BM];  // the two column halves of the row
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&bars->z_empty[t][ob]);
         }
         const int row = tc.qblk * (NQT * BM) + t * BM + r;
         const bool live = row < p.seqlen_q;
         const bool partial = PEER || p.part_num != nullptr;
-        const float den = NORM == FS_NORM_SIGNED_L1 ? zr + p.eps : sqrtf(zr + p.eps);
+        const float zr = raw * fd.zrep;  // z in the reference's units (bad-row report, partials)
+        const float den = NORM == FS_NORM_SIGNED_L1 ? raw + fd.eps_f : sqrtf(raw + fd.eps_f);
         // partial mode: the unnormalised numerator (the combine step divides by b(sum z + eps))
-        float mul = partial ? p.out_mul : __fdiv_rn(p.out_mul, den);
+        float mul = partial ? fd.out_mul : __fdiv_rn(fd.out_sgn, den);
         // partial row index: ((split * B + batch) * H + head) * Nq + row
         const int64_t prow =
             ((static_cast<int64_t>(tc.split) * p.n_batch + tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
@@ -903,7 +949,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           z_dst = base + static_cast<int64_t>(p.peer_world) * rows_slot * D + loc;
         }
         // row status once O's first columns are in: FP16 P overflow (inf) makes every O element
-        // non-finite, so one column tells; it is reported as z = +inf like a saturated FP8 P
+        // non-finite, so one column tells -- but only a row whose raw z reaches the overflow range
+        // can have overflowed (a NaN / inf in V alone leaves z below it and is passed through, as
+        // the reference does); it is reported as z = +inf like a saturated FP8 P
         auto finish_row = [&](bool ovf_o) {
           const float z_report = ovf_o ? __int_as_float(0x7f800000) : zr;
           const bool bad = !partial && (ovf_o || !(den > 0.f) || isinf(den));
@@ -944,8 +992,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < 32; ++i) acc[i] = 0u;
           }
           if (c == 0) {
-            const float a0 = __uint_as_float(acc[0]);
-            finish_row(TR::INF_CHECK && !isfinite(a0) && isfinite(zr));
+            // FP16 P overflow: an inf P_ij makes EVERY column of O_i non-finite (inf * v, or
+            // inf * 0 = NaN) and needs raw z >= (65504/p)^2.  Rows passing both cheap tests (column
+            // 0 non-finite, z in range) are confirmed by scanning all columns, so a NaN / inf in
+            // V alone (some columns) is passed through unflagged, as the reference does.
+            bool suspect = false;
+            if constexpr (TR::INF_CHECK) {
+              const float a0 = __uint_as_float(acc[0]);
+              suspect = tc.L > 0 && !isfinite(a0) && isfinite(raw) && raw >= ovf_raw;
+              if (__any_sync(0xffffffffu, suspect)) {  // warp-uniform: tcgen05.ld is warp-collective
+                uint32_t w[32];
+#pragma unroll 1
+                for (int c2 = 0; c2 < D / 32; ++c2) {
+                  if (c2 > 0) {
+                    ptx::tmem_ld32(o_addr + c2 * 32, w);
+                    ptx::tmem_wait_ld();
+                  }
+                  const uint32_t* src = c2 == 0 ? acc : w;
+#pragma unroll
+                  for (int i = 0; i < 32; ++i)
+                    if (c2 * 32 + i < p.head_dim && isfinite(__uint_as_float(src[i]))) suspect = false;
+                }
+              }
+            }
+            finish_row(suspect);
           }
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = (mul == 0.f) ? 0.f : __uint_as_float(acc[i]) * mul;
@@ -989,6 +1059,8 @@ static fs_status fail(fs_status st, const std::string& msg) {
   return st;
 }
 
+void set_last_error(const char* msg) { g_last_error = msg; }
+
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -1002,9 +1074,76 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
+constexpr int kMaxDevices = 64;
+
+// Encoded TMA descriptors, cached per thread: repeated calls on the same buffers (a layer loop,
+// a benchmark, a GRN forward) skip cuTensorMapEncodeTiled.  Key = everything the encode reads.
+struct TmaKey {
+  const void* ptr;
+  int64_t dims[4], strides[3];
+  int32_t box_w, box_rows, dt, swizzle, dev;
+  bool operator==(const TmaKey& o) const { return std::memcmp(this, &o, sizeof(TmaKey)) == 0; }
+};
+struct TmaCache {
+  static constexpr int N = 32;
+  TmaKey key[N];
+  CUtensorMap map[N];
+  uint64_t stamp[N] = {0};
+  uint64_t clock = 0;
+  const CUtensorMap* find(const TmaKey& k) {
+    for (int i = 0; i < N; ++i)
+      if (stamp[i] != 0 && key[i] == k) {
+        stamp[i] = ++clock;
+        return &map[i];
+      }
+    return nullptr;
+  }
+  void put(const TmaKey& k, const CUtensorMap& m) {
+    int v = 0;
+    for (int i = 1; i < N; ++i)
+      if (stamp[i] < stamp[v]) v = i;
+    key[v] = k;
+    map[v] = m;
+    stamp[v] = ++clock;
+  }
+};
+static thread_local TmaCache g_tma_cache;
+
+static bool encode_bshd_uncached(CUtensorMap* map, CUtensorMapDataType dt, int eb, const void* ptr, int head_dim,
+                                 int seqlen, int heads, int batch, const int64_t* stride, int box_w, int box_rows,
+                                 std::string* err, int swizzle);
+
 static bool encode_bshd(CUtensorMap* map, CUtensorMapDataType dt, int eb, const void* ptr, int head_dim, int seqlen,
                         int heads, int batch, const int64_t* stride, int box_w, int box_rows, std::string* err,
                         int swizzle = 128) {
+  TmaKey k;
+  std::memset(&k, 0, sizeof(k));  // padding bytes take part in the comparison
+  k.ptr = ptr;
+  k.dims[0] = head_dim;
+  k.dims[1] = seqlen;
+  k.dims[2] = heads;
+  k.dims[3] = batch;
+  k.strides[0] = stride[0] * eb;
+  k.strides[1] = stride[1] * eb;
+  k.strides[2] = stride[2] * eb;
+  k.box_w = box_w;
+  k.box_rows = box_rows;
+  k.dt = static_cast<int32_t>(dt);
+  k.swizzle = swizzle;
+  cudaGetDevice(&k.dev);
+  if (const CUtensorMap* hit = g_tma_cache.find(k)) {
+    *map = *hit;
+    return true;
+  }
+  if (!encode_bshd_uncached(map, dt, eb, ptr, head_dim, seqlen, heads, batch, stride, box_w, box_rows, err, swizzle))
+    return false;
+  g_tma_cache.put(k, *map);
+  return true;
+}
+
+static bool encode_bshd_uncached(CUtensorMap* map, CUtensorMapDataType dt, int eb, const void* ptr, int head_dim,
+                                 int seqlen, int heads, int batch, const int64_t* stride, int box_w, int box_rows,
+                                 std::string* err, int swizzle) {
   auto enc = get_encode_fn();
   if (!enc) {
     *err = "cuTensorMapEncodeTiled unavailable (driver too old?)";
@@ -1054,19 +1193,19 @@ static bool encode_key_scale(CUtensorMap* map, const fs_fwd_params* p, std::stri
 
 // SM count of the current device (persistent grid size), cached per device.
 static int num_sms() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[kMaxDevices];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  if (dev < 0 || dev >= 64) {
+  if (dev < 0 || dev >= kMaxDevices) {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }
-  if (cache[dev] == 0) {
+  if (cache[dev].load(std::memory_order_relaxed) == 0) {
     int n = 0;
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) cache[dev] = n;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) cache[dev].store(n);
   }
-  return cache[dev];
+  return cache[dev].load(std::memory_order_relaxed);
 }
 
 // K/V split plan: requested splits clamped to [1, n_kv_tiles], then every split non-empty.
@@ -1257,13 +1396,17 @@ template <int IN, int D, int OUT, int NORM, bool KS, bool PEER = false>
 static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   using C = Cfg<IN, D, KS>;
   auto kern = flashsign_fwd_kernel<IN, D, OUT, NORM, KS, PEER>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess)
-    return fail(FS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+  // the >48 KB dynamic shared-memory opt-in is per device (context): set it once per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return fail(FS_ERR_CUDA, "cudaGetDevice failed or device index out of range");
+  static std::atomic<bool> attr_set[kMaxDevices];
+  if (!attr_set[dev].load(std::memory_order_acquire)) {
+    cudaError_t attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (attr_err != cudaSuccess)
+      return fail(FS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+    attr_set[dev].store(true, std::memory_order_release);
+  }
 
   const CUtensorMapDataType dt = (IN == FS_BF16)  ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                  : (IN == FS_F16) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -1291,14 +1434,14 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   kp.seqlen_q = p->seqlen_q;
   kp.seqlen_kv = p->seqlen_kv;
   kp.head_dim = p->head_dim;
-  const double g = (double)p->scale * p->q_descale * p->k_descale;
-  kp.zmul = (float)(NORM == FS_NORM_SIGNED_L1 ? std::fabs(g) : g * g);
-  kp.out_mul = (float)(g * p->v_descale / p->p_scale);
+  kp.scale = p->scale;
   kp.eps = p->eps;
+  kp.q_descale = p->q_descale;
+  kp.k_descale = p->k_descale;
+  kp.v_descale = p->v_descale;
   kp.p_scale = p->p_scale;
+  kp.dev_scales = p->dev_scales;
   kp.bad_key = p->bad_key;
-  const double pmax = InTraits<IN>::PMAX / std::fabs((double)p->p_scale);
-  kp.ovf_z = (float)std::fmin(NORM == FS_NORM_SIGNED_L1 ? pmax : pmax * pmax, 3.0e38);
   const SplitPlan sp = split_plan(p);
   const int64_t n_qblk = (p->seqlen_q + NQT * BM * CL - 1) / (NQT * BM * CL);  // per cluster
   const int64_t n_tiles = n_qblk * sp.splits * p->heads_q * p->batch;
@@ -1340,16 +1483,13 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
     cfg.numAttrs = 1;
     // persistent grid: never more clusters than can be co-resident (a GPC with an odd SM count
     // holds one pair fewer), or the surplus clusters would run as a second wave
-    static int max_clusters[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev >= 0 && dev < 64) {
-      if (max_clusters[dev] == 0) {
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) max_clusters[dev] = n;
-      }
-      if (max_clusters[dev] > 0) grid = std::min(grid, max_clusters[dev] * CL);
+    static std::atomic<int> max_clusters[kMaxDevices];
+    if (max_clusters[dev].load(std::memory_order_relaxed) == 0) {
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) max_clusters[dev].store(n);
     }
+    const int mc = max_clusters[dev].load(std::memory_order_relaxed);
+    if (mc > 0) grid = std::min(grid, mc * CL);
     cfg.gridDim = dim3(grid);
     e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tm, kp);
   } else {

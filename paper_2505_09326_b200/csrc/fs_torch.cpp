@@ -1,0 +1,226 @@
+// fs_torch.cpp -- PyTorch C++ extension over the FlashSign C-ABI (include/flashsign.h).
+//
+// The torch-native entry `flashsign.fwd_async` (the batched, device-resident form of the
+// reference's multi_head_attention_array, attention.py:318-361) lands here: tensor checks,
+// output / bad-row-key / split-workspace allocation, the automatic K/V split choice and the
+// fs_fwd call all happen in C++ on the caller's current CUDA stream, so a call costs a few
+// microseconds of host time (the TMA descriptors are cached inside libflashsign.so).
+// The extension holds no kernels: it links libflashsign.so ($ORIGIN rpath) and calls the C-ABI,
+// exactly what an external binding would do.
+
+#include <ATen/cuda/CUDAContext.h>
+#include <c10/cuda/CUDAGuard.h>
+#include <torch/extension.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+#include "../../include/flashsign.h"
+
+namespace {
+
+int in_code(at::ScalarType t) {
+  switch (t) {
+    case at::kHalf: return FS_F16;
+    case at::kBFloat16: return FS_BF16;
+    case at::kFloat8_e4m3fn: return FS_E4M3;
+    default: return -1;
+  }
+}
+int out_code(at::ScalarType t) {
+  switch (t) {
+    case at::kHalf: return FS_F16;
+    case at::kBFloat16: return FS_BF16;
+    case at::kFloat: return FS_F32;
+    default: return -1;
+  }
+}
+
+// Python raises the mapped exception (ShapeMismatchError / ConfigError / RuntimeError) from the
+// status; validation failures detected here use the same codes.
+struct Fail {
+  int status;
+  std::string msg;
+};
+
+int sm_count(int dev) {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  std::lock_guard<std::mutex> g(mu);
+  if (dev < 0 || dev >= 64) return at::cuda::getDeviceProperties(dev)->multiProcessorCount;
+  if (cache[dev] == 0) cache[dev] = at::cuda::getDeviceProperties(dev)->multiProcessorCount;
+  return cache[dev];
+}
+
+// K/V splits for launches whose (b, h, 256-row) work tiles cannot fill the GPU: the wave model of
+// flashsign.auto_splits (one unit = one K/V tile step of one work tile; +2 per work tile for its
+// prologue / epilogue; plus the combine pass reading S partial rows of d+1 fp32).
+int auto_splits(int64_t b, int64_t h, int64_t nq, int64_t nkv, int d, int sms) {
+  const int64_t tiles = ((nq + 255) / 256) * h * b;
+  const int64_t n_kv = (nkv + 127) / 128;
+  if (tiles == 0 || tiles >= sms || n_kv < 8) return 1;
+  const int dk = d > 64 ? 128 : 64;
+  const double step_s = 4.0 * 256 * 128 * dk / 8.0e12;
+  const double rows = static_cast<double>(b * h * nq);
+  int best = 1;
+  double best_cost = 1e300;
+  const int64_t smax = std::min<int64_t>(16, n_kv / 4);
+  for (int64_t s = 1; s <= smax; ++s) {
+    const int64_t split_tiles = (n_kv + s - 1) / s;
+    const int64_t s_eff = (n_kv + split_tiles - 1) / split_tiles;
+    const int64_t waves = (tiles * s_eff + sms - 1) / sms;
+    const double comb = s_eff == 1 ? 0.0 : s_eff * rows * (dk + 1) * 4 / 5.0e12 / step_s;
+    const double cost = static_cast<double>(waves * (split_tiles + 2)) + comb;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = static_cast<int>(s);
+    }
+  }
+  return best;
+}
+
+void check_bshd(const at::Tensor& t, const char* name) {
+  if (!t.is_cuda()) throw Fail{FS_ERR_CUDA, std::string("flashsign: ") + name + " must be a CUDA tensor (no CPU fallback)"};
+  if (t.dim() != 4) throw Fail{FS_ERR_SHAPE, std::string("flashsign: ") + name + " must be BSHD rank-4"};
+  if (t.stride(3) != 1) throw Fail{FS_ERR_SHAPE, std::string("flashsign: ") + name + " head dim must be contiguous"};
+}
+
+// Returns (status, message, out, bad_key, partial, n_parts).
+py::tuple fwd(const at::Tensor& q, const at::Tensor& k, const at::Tensor& v, c10::optional<at::Tensor> out,
+              c10::optional<at::ScalarType> out_dtype, c10::optional<at::Tensor> bad_key, double scale, double eps,
+              double p_scale, double q_descale, double k_descale, double v_descale, int64_t normalizer,
+              c10::optional<at::Tensor> key_scale, int64_t kv_splits, c10::optional<at::Tensor> partial,
+              bool partial_only, c10::optional<at::Tensor> dev_scales, int64_t tile_m, int64_t tile_n) {
+  try {
+    check_bshd(q, "q");
+    check_bshd(k, "k");
+    check_bshd(v, "v");
+    if (q.scalar_type() != k.scalar_type() || q.scalar_type() != v.scalar_type())
+      throw Fail{FS_ERR_SHAPE, "dtype mismatch: q, k, v must share a dtype"};
+    const int ic = in_code(q.scalar_type());
+    if (ic < 0) throw Fail{FS_ERR_SHAPE, "flashsign: unsupported input dtype (bf16, fp16, float8_e4m3fn)"};
+    if (q.device() != k.device() || q.device() != v.device())
+      throw Fail{FS_ERR_CUDA, "flashsign: q, k, v must be on the same device"};
+    const int64_t b = q.size(0), nq = q.size(1), h = q.size(2), d = q.size(3);
+    const int64_t nkv = k.size(1), hkv = k.size(2);
+    if (k.size(0) != b || v.size(0) != b) throw Fail{FS_ERR_SHAPE, "batch mismatch between q, k, v"};
+    if (k.size(3) != d) throw Fail{FS_ERR_SHAPE, "Q and K feature dims differ"};
+    if (v.size(1) != nkv || v.size(2) != hkv) throw Fail{FS_ERR_SHAPE, "K and V shapes differ"};
+    if (v.size(3) != d) throw Fail{FS_ERR_SHAPE, "flashsign: value dim must equal head dim"};
+    if (h < 1 || hkv < 1 || h % hkv != 0)
+      throw Fail{FS_ERR_CONFIG, "query heads must be a multiple of kv heads, got h=" + std::to_string(h) +
+                                    ", h_kv=" + std::to_string(hkv)};
+    if (!std::isfinite(scale)) throw Fail{FS_ERR_CONFIG, "score_scale must be finite"};
+    const c10::cuda::CUDAGuard guard(q.device());
+    const auto dev = q.device();
+    at::ScalarType odt;
+    if (out_dtype.has_value())
+      odt = *out_dtype;
+    else if (out.has_value())
+      odt = out->scalar_type();
+    else
+      odt = (q.scalar_type() == at::kHalf || q.scalar_type() == at::kBFloat16) ? q.scalar_type() : at::kBFloat16;
+    const int oc = out_code(odt);
+    if (oc < 0) throw Fail{FS_ERR_SHAPE, "flashsign: unsupported output dtype"};
+    at::Tensor o;
+    if (out.has_value()) {
+      o = *out;
+      if (o.dim() != 4 || o.size(0) != b || o.size(1) != nq || o.size(2) != h || o.size(3) != d ||
+          o.scalar_type() != odt || o.stride(3) != 1 || o.device() != dev)
+        throw Fail{FS_ERR_SHAPE, "flashsign: bad out tensor"};
+    } else {
+      o = at::empty({b, nq, h, d}, q.options().dtype(odt));
+    }
+    at::Tensor bad = bad_key.has_value() ? *bad_key : at::empty({1}, q.options().dtype(at::kLong));
+
+    fs_fwd_params p;
+    std::memset(&p, 0, sizeof(p));
+    p.q = q.data_ptr();
+    p.k = k.data_ptr();
+    p.v = v.data_ptr();
+    p.o = o.data_ptr();
+    for (int i = 0; i < 3; ++i) {
+      p.q_stride[i] = q.stride(i);
+      p.k_stride[i] = k.stride(i);
+      p.v_stride[i] = v.stride(i);
+      p.o_stride[i] = o.stride(i);
+    }
+    p.batch = static_cast<int32_t>(b);
+    p.heads_q = static_cast<int32_t>(h);
+    p.heads_kv = static_cast<int32_t>(hkv);
+    p.seqlen_q = static_cast<int32_t>(nq);
+    p.seqlen_kv = static_cast<int32_t>(nkv);
+    p.head_dim = static_cast<int32_t>(d);
+    p.in_dtype = static_cast<fs_dtype>(ic);
+    p.out_dtype = static_cast<fs_dtype>(oc);
+    p.scale = static_cast<float>(scale);
+    p.eps = static_cast<float>(eps);
+    p.p_scale = static_cast<float>(p_scale);
+    p.q_descale = static_cast<float>(q_descale);
+    p.k_descale = static_cast<float>(k_descale);
+    p.v_descale = static_cast<float>(v_descale);
+    p.bad_key = reinterpret_cast<uint64_t*>(bad.data_ptr());
+    p.tile_m_hint = static_cast<int32_t>(tile_m);
+    p.tile_n_hint = static_cast<int32_t>(tile_n);
+    p.normalizer = static_cast<int32_t>(normalizer);
+    auto stream = at::cuda::getCurrentCUDAStream(dev.index());
+    at::Tensor ks;
+    if (key_scale.has_value()) {
+      ks = key_scale->dim() == 2 ? *key_scale : key_scale->reshape({1, -1});
+      if (!ks.is_cuda() || ks.scalar_type() != at::kFloat || ks.device() != dev || ks.size(0) != b ||
+          ks.size(1) != nkv || (nkv > 0 && ks.stride(1) != 1))
+        throw Fail{FS_ERR_SHAPE, "flashsign: key_scale must be float32 [B, Nkv] on q's device with unit key stride"};
+      const bool aligned = (reinterpret_cast<uintptr_t>(ks.data_ptr()) % 16) == 0 &&
+                           (b == 1 || ((ks.stride(0) * 4) % 16 == 0 && ks.stride(0) >= nkv));
+      if (!aligned) {  // TMA needs 16-byte rows: aligned copy on this (the launch) stream
+        at::Tensor buf = at::zeros({b, std::max<int64_t>(4, (nkv + 3) / 4 * 4)}, ks.options());
+        buf.narrow(1, 0, nkv).copy_(ks);
+        ks = buf.narrow(1, 0, nkv);
+      }
+      p.key_scale = ks.data_ptr<float>();
+      p.key_scale_stride = ks.stride(0);
+    }
+    p.kv_splits = static_cast<int32_t>(
+        kv_splits >= 0 ? kv_splits : auto_splits(b, h, nq, nkv, static_cast<int>(d), sm_count(dev.index())));
+    p.partial_only = partial_only ? 1 : 0;
+    if (dev_scales.has_value()) {
+      const at::Tensor& ds = *dev_scales;
+      if (!ds.is_cuda() || ds.scalar_type() != at::kFloat || ds.numel() < 4 || !ds.is_contiguous() || ds.device() != dev)
+        throw Fail{FS_ERR_SHAPE, "flashsign: dev_scales must be a contiguous float32 CUDA tensor of 4 elements"};
+      p.dev_scales = ds.data_ptr<float>();
+    }
+    at::Tensor part;
+    int32_t n_parts = fs_kv_splits(&p);
+    if (partial_only || n_parts > 1) {
+      const int64_t need = fs_partial_floats(&p);
+      if (partial.has_value()) {
+        part = *partial;
+        if (part.scalar_type() != at::kFloat || part.numel() < need || !part.is_contiguous() || part.device() != dev)
+          throw Fail{FS_ERR_SHAPE, "flashsign: partial workspace needs " + std::to_string(need) +
+                                       " contiguous float32 elements"};
+      } else {
+        part = at::empty({need}, q.options().dtype(at::kFloat));
+      }
+      p.partial = part.data_ptr<float>();
+    }
+    const fs_status st = fs_fwd(&p, reinterpret_cast<fs_stream_t>(stream.stream()));
+    if (st != FS_OK) return py::make_tuple(static_cast<int>(st), std::string(fs_last_error()), py::none(),
+                                           py::none(), py::none(), 0);
+    return py::make_tuple(0, std::string(), o, bad, part.defined() ? py::cast(part) : py::none(), n_parts);
+  } catch (const Fail& f) {
+    return py::make_tuple(f.status, f.msg, py::none(), py::none(), py::none(), 0);
+  }
+}
+
+}  // namespace
+
+PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
+  m.doc() = "FlashSign torch binding over the C-ABI (include/flashsign.h)";
+  m.def("fwd", &fwd, "FlashSign forward on BSHD CUDA tensors (current stream)", py::arg("q"), py::arg("k"),
+        py::arg("v"), py::arg("out"), py::arg("out_dtype"), py::arg("bad_key"), py::arg("scale"), py::arg("eps"),
+        py::arg("p_scale"), py::arg("q_descale"), py::arg("k_descale"), py::arg("v_descale"),
+        py::arg("normalizer"), py::arg("key_scale"), py::arg("kv_splits"), py::arg("partial"),
+        py::arg("partial_only"), py::arg("dev_scales"), py::arg("tile_m"), py::arg("tile_n"));
+  m.def("version", []() { return fs_version(); });
+}

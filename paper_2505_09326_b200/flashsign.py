@@ -48,6 +48,7 @@ _STATUS_EXC = {
 }
 
 BAD_NONE = _lib.FS_BAD_NONE
+_ext = None  # the torch extension, bound on first use
 
 
 def _check_inputs(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
@@ -81,7 +82,8 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
               bad_key: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None,
               tile_hint: tuple[int, int] = (0, 0), normalizer: str = "spherical",
               key_scale: torch.Tensor | None = None, kv_splits: int | None = None,
-              partial: torch.Tensor | None = None, partial_only: bool = False):
+              partial: torch.Tensor | None = None, partial_only: bool = False,
+              dev_scales: torch.Tensor | None = None):
     """Launch FlashSign and return ``(o, bad_key)`` without synchronising.
 
     ``bad_key`` is a 1-element int64 CUDA tensor holding the packed first bad
@@ -93,79 +95,31 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
     (b, h, 256-row) work tiles cannot fill the GPU); ranges merge by plain addition
     of (numerator, z) (streaming.py:122-128), in a second small kernel.
     With ``partial_only`` the call returns ``(partial, n_parts)`` instead (see ``fwd_partial``).
+    ``dev_scales``: float32 CUDA tensor of 4 elements {q, k, v descale, p_scale} read by the kernel
+    instead of the host values (written on the device, e.g. by ``prepare``; no host round trip).
     """
-    _check_inputs(q, k, v)
     if normalizer not in NORMALIZERS:
         raise ConfigError(f"flashsign: normalizer must be one of {sorted(NORMALIZERS)} (exp-free), got {normalizer!r}")
-    if not math.isfinite(scale):
-        raise ConfigError(f"score_scale must be finite, got {scale}")
-    b, nq, h, d = q.shape
-    _, nkv, hkv, _ = k.shape
-    if h < 1 or hkv < 1 or h % hkv != 0:
-        raise ConfigError(f"query heads must be a multiple of kv heads, got h={h}, h_kv={hkv}")
-    if out_dtype is None:
-        out_dtype = out.dtype if out is not None else (torch.bfloat16 if q.dtype not in (torch.bfloat16, torch.float16)
-                                                       else q.dtype)
-    if out_dtype not in _OUT_CODES:
-        raise ShapeMismatchError(f"flashsign: unsupported output dtype {out_dtype}")
-    if out is None:
-        out = torch.empty((b, nq, h, d), dtype=out_dtype, device=q.device)
-    elif tuple(out.shape) != (b, nq, h, d) or out.dtype != out_dtype or out.stride(-1) != 1:
-        raise ShapeMismatchError(f"flashsign: bad out tensor {tuple(out.shape)} {out.dtype}")
-    if bad_key is None:
-        bad_key = torch.empty(1, dtype=torch.int64, device=q.device)
-
-    prm = _lib.FsFwdParams()
-    prm.q, prm.k, prm.v, prm.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
-    for dst, t in ((prm.q_stride, q), (prm.k_stride, k), (prm.v_stride, v), (prm.o_stride, out)):
-        dst[0], dst[1], dst[2] = t.stride(0), t.stride(1), t.stride(2)
-    prm.batch, prm.heads_q, prm.heads_kv = b, h, hkv
-    prm.seqlen_q, prm.seqlen_kv, prm.head_dim = nq, nkv, d
-    prm.in_dtype, prm.out_dtype = _IN_CODES[q.dtype], _OUT_CODES[out_dtype]
-    prm.scale, prm.eps, prm.p_scale = float(scale), float(eps), float(p_scale)
-    prm.q_descale, prm.k_descale, prm.v_descale = float(q_descale), float(k_descale), float(v_descale)
-    prm.bad_key = bad_key.data_ptr()
-    prm.tile_m_hint, prm.tile_n_hint = int(tile_hint[0]), int(tile_hint[1])
-    prm.normalizer = NORMALIZERS[normalizer]
-    if key_scale is not None:
-        ks = key_scale if key_scale.dim() == 2 else key_scale.reshape(1, -1)
-        if (not ks.is_cuda or ks.dtype != torch.float32 or ks.device != q.device
-                or tuple(ks.shape) != (b, nkv) or (nkv > 0 and ks.stride(1) != 1)):
-            raise ShapeMismatchError(f"flashsign: key_scale must be float32 [{b}, {nkv}] on {q.device} with unit "
-                                     f"key stride, got {tuple(key_scale.shape)} {key_scale.dtype}")
-        if (b > 1 and ((ks.stride(0) * 4) % 16 != 0 or ks.stride(0) < nkv)) or ks.data_ptr() % 16 != 0:
-            ks = _padded_rows(ks)
-        prm.key_scale, prm.key_scale_stride = ks.data_ptr(), ks.stride(0)
-        key_scale = ks  # keep alive until the launch is enqueued
-    prm.kv_splits = int(auto_splits(b, h, nq, nkv, q.device, d) if kv_splits is None else kv_splits)
-    if prm.kv_splits < 0:
+    if kv_splits is not None and kv_splits < 0:
         raise ConfigError(f"kv_splits must be >= 0, got {kv_splits}")
-    lib = _lib.load()
-    prm.partial_only = int(bool(partial_only))
-    if partial_only or lib.fs_kv_splits(ctypes.byref(prm)) > 1:
-        need = lib.fs_partial_floats(ctypes.byref(prm))
-        if partial is None:
-            partial = torch.empty(need, dtype=torch.float32, device=q.device)
-        elif partial.dtype != torch.float32 or partial.numel() < need or not partial.is_contiguous():
-            raise ShapeMismatchError(f"flashsign: partial workspace needs {need} contiguous float32 elements")
-        prm.partial = partial.data_ptr()
-
+    # validation, allocation, the split choice and fs_fwd run in the C++ extension (csrc/fs_torch.cpp)
+    args = (q, k, v, out, out_dtype, bad_key, float(scale), float(eps), float(p_scale), float(q_descale),
+            float(k_descale), float(v_descale), NORMALIZERS[normalizer], key_scale,
+            -1 if kv_splits is None else int(kv_splits), partial, bool(partial_only), dev_scales,
+            int(tile_hint[0]), int(tile_hint[1]))
+    global _ext
+    ext = _ext or _lib.load_torch_ext()
+    _ext = ext
     if stream is None:
-        with torch.cuda.device(q.device):
-            stream = torch.cuda.current_stream()
+        st, msg, o, bad, part, n_parts = ext.fwd(*args)
     else:
-        # buffers allocated here on the current stream but used on `stream`: keep the caching
-        # allocator from recycling them before `stream` is done with them
-        for t in (out, bad_key, partial, key_scale):
-            if t is not None:
-                t.record_stream(stream)
-    with torch.cuda.device(q.device):  # the C-ABI launches on the current device
-        st = lib.fs_fwd(ctypes.byref(prm), ctypes.c_void_p(stream.cuda_stream))
-    if st != _lib.FS_OK:
-        raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
+        with torch.cuda.stream(stream):  # buffers the call allocates come from `stream` itself
+            st, msg, o, bad, part, n_parts = ext.fwd(*args)
+    if st:
+        raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {msg}")
     if partial_only:
-        return partial, lib.fs_kv_splits(ctypes.byref(prm))
-    return out, bad_key
+        return part, n_parts
+    return o, bad
 
 
 _SMS: dict = {}
@@ -333,3 +287,53 @@ class CapturedFwd:
     def replay(self) -> torch.Tensor:
         self.graph.replay()
         return self.out
+
+
+_SRC_CODES = {torch.float32: _lib.FS_F32, torch.float64: _lib.FS_F64, torch.float16: _lib.FS_F16,
+              torch.bfloat16: _lib.FS_BF16}
+
+
+def prepare(srcs, dsts, *, stats: torch.Tensor, scales: torch.Tensor, scale: float = 1.0, eps: float = 0.0,
+            normalizer: str = "spherical", exact: bool = False, stream: torch.cuda.Stream | None = None) -> None:
+    """Convert caller tensors to kernel operands with device-chosen power-of-two scales (C-ABI
+    ``fs_prepare``, include/flashsign.h).  ``srcs`` / ``dsts``: three entries (q, k, v), each a 2-D
+    CUDA tensor ``[rows, d]`` / ``[rows, d_pad]`` with unit column stride, or ``None`` to reuse that
+    slot's stats from an earlier call on the same ``stats`` workspace (float64, 6 elements).
+    ``scales`` (float32, 4 elements) receives {q, k, v descale, p_scale} for ``fwd_async(dev_scales=)``.
+    Async on ``stream`` (default: current)."""
+    prm = _lib.FsPrepParams()
+    dst_dtype = d_pad = dev = None
+    for i, (x, y) in enumerate(zip(srcs, dsts)):
+        if x is None:
+            continue
+        if x.dim() != 2 or y is None or y.dim() != 2 or x.stride(1) != 1 or y.stride(1) != 1:
+            raise ShapeMismatchError("flashsign.prepare: 2-D tensors with unit column stride expected")
+        if x.dtype not in _SRC_CODES or y.dtype not in _IN_CODES or x.shape[0] != y.shape[0]:
+            raise ShapeMismatchError(f"flashsign.prepare: bad dtypes/rows {x.dtype} {tuple(x.shape)} -> "
+                                     f"{y.dtype} {tuple(y.shape)}")
+        if dst_dtype is not None and (y.dtype != dst_dtype or y.shape[1] != d_pad):
+            raise ShapeMismatchError("flashsign.prepare: every operand must share dtype and padded width")
+        dst_dtype, d_pad, dev = y.dtype, y.shape[1], x.device
+        t = prm.t[i]
+        t.src, t.src_dtype, t.d, t.rows = x.data_ptr(), _SRC_CODES[x.dtype], x.shape[1], x.shape[0]
+        t.src_row_stride, t.dst, t.dst_row_stride = x.stride(0), y.data_ptr(), y.stride(0)
+    if dst_dtype is None:
+        raise ShapeMismatchError("flashsign.prepare: no tensor given")
+    if stats.dtype != torch.float64 or stats.numel() < 6 or scales.dtype != torch.float32 or scales.numel() < 4:
+        raise ShapeMismatchError("flashsign.prepare: stats float64[6] and scales float32[4] workspaces expected")
+    prm.dst_dtype, prm.d_pad = _IN_CODES[dst_dtype], d_pad
+    prm.mode = _lib.FS_PREP_EXACT if exact else _lib.FS_PREP_SCALE
+    prm.normalizer = NORMALIZERS[normalizer]
+    prm.scale, prm.eps = float(scale), float(eps)
+    prm.stats, prm.scales = stats.data_ptr(), scales.data_ptr()
+    with torch.cuda.device(dev):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        st = _lib.load().fs_prepare(ctypes.byref(prm), ctypes.c_void_p(s.cuda_stream))
+    if st != _lib.FS_OK:
+        raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
+
+
+def kernel_score_tile(head_dim: int, dtype: torch.dtype = torch.bfloat16) -> int:
+    """Scores the kernel holds on chip per Q tile (128 rows x 128 / 192 keys, in TMEM)."""
+    bm, bn = _lib.query_tile(min(max(head_dim, 1), 128), _IN_CODES[dtype])
+    return bm * bn

@@ -11,10 +11,13 @@ the reference's (e.g. for callers that evaluate ``spec.a2`` themselves).
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field, replace
 from typing import Callable
 
 import numpy as np
+
+from ._reftypes import ref_type
 
 PROPERTY_FLAGS = frozenset({"sign_preserving", "shift_invariant", "positive_scale_invariant"})
 
@@ -30,6 +33,11 @@ class DegenerateDenominatorError(ValueError):
         self.z = z
         text = f"degenerate denominator: b applied to z={z!r} is zero or non-finite"
         super().__init__(text + (f" ({context})" if context else ""))
+
+
+if ref_type("DegenerateDenominatorError") is not None:
+    # the reference's own class (normalizers.py:29-35): `except ncstream...` matches the GPU path
+    DegenerateDenominatorError = ref_type("DegenerateDenominatorError")  # noqa: F811
 
 
 def _identity(u):
@@ -69,6 +77,19 @@ class NormalizerSpec:
 
     def with_epsilon(self, eps: float) -> "NormalizerSpec":
         return replace(self, denom_epsilon=eps)
+
+    def denominator(self, z, context: str = ""):
+        """b(z + denom_epsilon), raising DegenerateDenominatorError when it is unusable
+        (normalizers.py:83-91: a scalar must be finite and nonzero; an array must not
+        compare equal to 0 -- the reference's own truth test, so a multi-element array
+        raises numpy's ambiguity ValueError exactly as there)."""
+        den = self.b(z + self.denom_epsilon) if self.denom_epsilon else self.b(z)
+        if isinstance(den, (int, float, np.floating)):
+            if not math.isfinite(den) or den == 0:
+                raise DegenerateDenominatorError(z, context)
+        elif den == 0:
+            raise DegenerateDenominatorError(z, context)
+        return den
 
 
 SPHERICAL = NormalizerSpec("spherical", _identity, _square, _sqrt,

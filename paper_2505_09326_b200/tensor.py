@@ -8,12 +8,18 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._reftypes import ref_type
+
 DTYPES = {"float32": np.float32, "float64": np.float64}
 FLOAT16_MAX = 65504.0
 
 
 class ShapeMismatchError(ValueError):
     """Incompatible operand shapes or dtypes (tensor.py:32-33)."""
+
+
+if ref_type("ShapeMismatchError") is not None:
+    ShapeMismatchError = ref_type("ShapeMismatchError")  # noqa: F811  (ncstream's own class)
 
 
 class DenseTensor:
@@ -61,6 +67,10 @@ class DenseTensor:
 
     def __repr__(self) -> str:
         return f"DenseTensor(shape={self.shape}, dtype={self._dtype})"
+
+
+if ref_type("DenseTensor") is not None:
+    DenseTensor = ref_type("DenseTensor")  # noqa: F811  (the wrappers return ncstream's carrier)
 
 
 def quantize_f16_array(arr: np.ndarray) -> np.ndarray:

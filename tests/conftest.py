@@ -8,6 +8,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+# the reference install (baseline/install_ref.sh): drop-in type identity + the reference arm
+if os.path.isdir(os.path.join(REF_INSTALL, "ncstream")) and REF_INSTALL not in sys.path:
+    sys.path.append(REF_INSTALL)
+
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.npz")
 
 

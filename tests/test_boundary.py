@@ -52,7 +52,8 @@ def test_library_is_sm100a_with_tcgen05():
     assert "HMMA" not in re.sub(r"UTC[HQ]MMA", "", sass)  # no legacy mma.sync path
 
 
-@pytest.mark.parametrize("cname,cls", [("fs_fwd_params", _lib.FsFwdParams), ("fs_peer_params", _lib.FsPeerParams)])
+@pytest.mark.parametrize("cname,cls", [("fs_fwd_params", _lib.FsFwdParams), ("fs_peer_params", _lib.FsPeerParams),
+                                       ("fs_prep_tensor", _lib.FsPrepTensor), ("fs_prep_params", _lib.FsPrepParams)])
 def test_struct_layout_matches_header(tmp_path, cname, cls):
     fields = [f[0] for f in cls._fields_]
     prog = tmp_path / "layout.c"

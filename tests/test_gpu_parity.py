@@ -378,16 +378,19 @@ def test_compat_criterion4_accuracy(golden, compute, frac):
     assert within >= frac, within
 
 
-def test_compat_meter_records_kernel_tile():
-    from paper_2505_09326_b200 import SPHERICAL
+def test_compat_meter_records_reference_tile_contract():
+    # the reference's contract, min(g_y, y) * min(s_x, x) (test_attention.py:149-157; 1 for the
+    # scalar 1x1 path, attention.py:217-218); the kernel's own on-chip tile is reported separately
+    from paper_2505_09326_b200 import SPHERICAL, flashsign
     at = compat()
     rng = np.random.default_rng(7)
-    for y, x in [(16, 16), (97, 33), (5, 400), (300, 300)]:
+    for (y, x, g, s) in [(16, 16, 4, 4), (97, 33, 13, 7), (5, 400, 64, 64), (8, 8, 64, 64), (300, 300, 1, 1)]:
         m = at.ScoreBufferMeter()
         at.streamed_attention_array(rng.standard_normal((y, 64)), rng.standard_normal((x, 64)),
-                                    rng.standard_normal((x, 64)), SPHERICAL, 1.0, at.TileConfig(8, 8), meter=m)
-        bm, bn = __import__("paper_2505_09326_b200")._lib.query_tile(64, 1)  # the kernel's tile (d=64)
-        assert m.peak_elements == min(bm, y) * min(bn, x)
+                                    rng.standard_normal((x, 64)), SPHERICAL, 1.0, at.TileConfig(g, s), meter=m)
+        assert m.peak_elements == (1 if (g, s) == (1, 1) else min(g, y) * min(s, x))
+    assert flashsign.kernel_score_tile(64, torch.bfloat16) == 128 * 192
+    assert flashsign.kernel_score_tile(128, torch.bfloat16) == 128 * 128
 
 
 def test_compat_empty_query_returns_empty():
