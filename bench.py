@@ -702,12 +702,13 @@ def run_ours(args, cfg):
             rows = args.cpu_rows or reference_rows(cfg)
             with _all_host_threads():
                 tt_, ff_ = 0.0, 0.0
+                cpu_reference_sample(cfg, rows, seed=6)  # warm-up, like the reference arm's
                 for rep_ in range(3):  # same sample as one step of the reference arm, three times
                     dt, fl, threads, kind, what = cpu_reference_sample(cfg, rows, seed=7 + rep_)
                     tt_, ff_ = tt_ + dt, ff_ + fl
                 host = _host_info()
             cpu = {"value": ff_ / tt_ / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
-                   "sample": f"3 x ({rows} query positions x {H} heads x {N} keys x d{D} of one batch element), "
+                   "sample": f"1 warm-up + 3 x ({rows} query positions x {H} heads x {N} keys x d{D} of one batch element), "
                              f"float32 holding {cfg['dtype']} values, tile 64x64: {what}; {tt_:.2f} s",
                    "cpu_count": os.cpu_count(), **host}
         ctx = None

@@ -167,11 +167,8 @@ def context_parallel_fwd_peer(q: torch.Tensor, k_shard: torch.Tensor, v_shard: t
         if st != _lib.FS_OK:
             raise flashsign._STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
     lo, hi = peer_rows(nq, world, rank)
-    if check:
-        info = flashsign.decode_bad_key(int(bad.item()), h, nq)
-        if info is not None:
-            from .normalizers import DegenerateDenominatorError
-            raise DegenerateDenominatorError(float(info[3]), f"row {info[2]}")
+    # collectives first, on every rank, before anything may raise (no rank can leave the others
+    # blocked in all_gather / all_reduce)
     if gather and world > 1:
         r = pp.rows_per_rank
         mine = torch.zeros((b, r, h, d), dtype=out.dtype, device=out.device)
@@ -181,6 +178,19 @@ def context_parallel_fwd_peer(q: torch.Tensor, k_shard: torch.Tensor, v_shard: t
         for src, part in enumerate(parts):
             plo, phi = peer_rows(nq, world, src)
             out[:, plo:phi] = part[:, :phi - plo]
+    if check:
+        key = bad
+        if world > 1:
+            # every rank raises for the same, globally first bad row: MIN over the packed keys,
+            # compared unsigned (xor of the sign bit maps unsigned order onto signed order)
+            flip = torch.iinfo(torch.int64).min
+            key = torch.bitwise_xor(bad, flip)
+            dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+            key = torch.bitwise_xor(key, flip)
+        info = flashsign.decode_bad_key(int(key.item()), h, nq)
+        if info is not None:
+            from .normalizers import DegenerateDenominatorError
+            raise DegenerateDenominatorError(float(info[3]), f"row {info[2]}")
     return out, (lo, hi)
 
 

@@ -438,6 +438,31 @@ def test_full_size_config_against_gram_oracle(cfg):
         check_tol(o[b, :, h].float().cpu().numpy(), ref, dt, f"{name} b{b} h{h}")
 
 
+@pytest.mark.parametrize("name,fused", [("c2", False), ("c3", False), ("c4", False), ("c5", False), ("c5", True)],
+                         ids=["c2", "c3", "c4", "c5-prescaled", "c5-key_scale"])
+def test_full_size_as_benchmarked(name, fused):
+    """The configurations exactly as bench.py runs them: full batch, full N, the bench's own
+    inputs (bench.make_inputs, seeded per unit), C5 with its multiplicities m in {0..5} and
+    eps = 1e-6 -- pre-scaled K' = m K (the default bench line) and fused in-kernel (key_scale,
+    --fused-mult).  Slices from the first, middle and LAST batch rows are checked in float64."""
+    import bench
+    cfg = dict(bench.CONFIGS[name])
+    if fused:
+        cfg["fused_mult"] = True
+    B, H, N, D = cfg["B"], cfg["H"], cfg["N"], cfg["D"]
+    q, k, v, m, _ = bench.make_inputs(cfg, 0, B * cfg["HKV"], torch.device("cuda"))
+    dt = q.dtype
+    o = fs().fwd(q, k, v, eps=cfg["eps"], key_scale=m)
+    for b, h in [(0, 0), (B // 2, H // 2), (B - 1, H - 1), (B - 1, 0)]:
+        kb = k[b, :, h].float().cpu().numpy().astype(np.float64)
+        if m is not None:
+            kb = kb * m[b].cpu().numpy().astype(np.float64)[:, None]
+        ref = gram_spherical(q[b, :, h].float().cpu().numpy(), kb, v[b, :, h].float().cpu().numpy(), 1.0, cfg["eps"])
+        check_tol(o[b, :, h].float().cpu().numpy(), ref, dt, f"{name} b{b} h{h}")
+    del q, k, v, o
+    torch.cuda.empty_cache()
+
+
 def test_host_pipeline_equals_device_path():
     from paper_2505_09326_b200.pipeline import HostPipeline
     q = rand_bshd(5, 700, 4, 128, torch.bfloat16, 50)
