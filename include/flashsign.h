@@ -93,7 +93,9 @@ typedef struct {
      S > 1 cuts every (b, h) K/V stream into S contiguous ranges computed by independent work
      tiles (for small B*H with long N); partial numerators and z go to `partial` and fs_fwd then
      runs the combine kernel (O = sum_s num_s / b(sum_s z_s + eps)) on the same stream.
-     fs_kv_splits(p) returns the effective S (clamped so that every range is non-empty). */
+     fs_kv_splits(p) returns the effective S (clamped so that every range is non-empty).
+     FS_SPLITS_AUTO (-1): the library picks S and split_tail from its wave model of the persistent
+     grid on the current device (fs_plan); size `partial` with fs_partial_floats(p). */
   int32_t kv_splits;
   /* Optional per-key multiplicity m (NULL: none): fp32 device array [batch, seqlen_kv],
      element (b, n) at key_scale[b*key_scale_stride + n], shared by all kv heads -- the
@@ -110,12 +112,19 @@ typedef struct {
      runs its K/V shard with partial_only = 1, the ranks all-reduce(sum) `partial`, then each
      calls fs_combine(p, 1, stream) to normalise. */
   int32_t partial_only;
-  int32_t reserved1; /* must be 0 */
+  /* 0: every work tile is split into kv_splits K/V ranges (uniform).  1: only the work tiles of
+     the persistent grid's last, partial wave are split (tiles = W*G + T over G co-resident
+     clusters of 2 CTAs, each 512 query rows of one (b, h); the T tail tiles become T*S items), so
+     the last wave keeps every SM busy; `partial` then holds S*T*512 rows.  Ignored with
+     partial_only.  (Was reserved1, required 0.) */
+  int32_t split_tail;
   /* Optional device array of 4 floats {q_descale, k_descale, v_descale, p_scale} (NULL: the host
      fields above).  Read by the kernel at launch time, so per-tensor scales chosen on the device
      (fs_prepare, below) need no host round trip.  Same constraints as the host fields. */
   const float *dev_scales;
 } fs_fwd_params;
+
+#define FS_SPLITS_AUTO (-1)
 
 /* Validate, encode TMA descriptors (cached per call), launch.  Async. */
 fs_status fs_fwd(const fs_fwd_params *p, fs_stream_t stream);
@@ -123,6 +132,18 @@ fs_status fs_fwd(const fs_fwd_params *p, fs_stream_t stream);
 /* Effective number of K/V ranges for p (>= 1) and the partial workspace size in floats. */
 int32_t fs_kv_splits(const fs_fwd_params *p);
 int64_t fs_partial_floats(const fs_fwd_params *p);
+
+/* The split plan fs_fwd would use for p (host only when clusters > 0: plan for that many
+   co-resident 2-CTA clusters, e.g. 74 on a 148-SM B200; 0 = query the current device), and the
+   wave model's result: items are walked by the clusters with a static stride (item i on cluster
+   i % G), busiest_steps = K/V-tile steps on the most loaded cluster, efficiency = all steps /
+   (G * busiest_steps). */
+typedef struct {
+  int32_t splits, split_tail, clusters, n_whole, tail_tiles, n_kv_tiles;
+  int64_t work_tiles, items, partial_floats;
+  double busiest_steps, efficiency;
+} fs_plan_info;
+fs_status fs_plan(const fs_fwd_params *p, int32_t clusters, fs_plan_info *out);
 
 /* O = sum_s num_s / b(sum_s z_s + eps) over the first n_parts partials in p->partial, written to
    p->o with p->o_stride / out_dtype, and the bad-row key (reset first) -- the merge step of the

@@ -23,7 +23,8 @@ FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
 # every symbol include/flashsign.h declares
 EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version", "fs_kv_splits", "fs_partial_floats",
                     "fs_combine", "fs_peer_floats", "fs_fwd_peer", "fs_combine_peer", "fs_ipc_malloc", "fs_ipc_open",
-                    "fs_ipc_close", "fs_ipc_free", "fs_prepare")
+                    "fs_ipc_close", "fs_ipc_free", "fs_prepare", "fs_plan")
+FS_SPLITS_AUTO = -1
 
 
 class FsFwdParams(ctypes.Structure):
@@ -61,8 +62,26 @@ class FsFwdParams(ctypes.Structure):
         ("key_scale_stride", ctypes.c_int64),
         ("partial", ctypes.c_void_p),
         ("partial_only", ctypes.c_int32),
-        ("reserved1", ctypes.c_int32),
+        ("split_tail", ctypes.c_int32),
         ("dev_scales", ctypes.c_void_p),
+    ]
+
+
+class FsPlanInfo(ctypes.Structure):
+    """Mirror of ``fs_plan_info`` (include/flashsign.h)."""
+
+    _fields_ = [
+        ("splits", ctypes.c_int32),
+        ("split_tail", ctypes.c_int32),
+        ("clusters", ctypes.c_int32),
+        ("n_whole", ctypes.c_int32),
+        ("tail_tiles", ctypes.c_int32),
+        ("n_kv_tiles", ctypes.c_int32),
+        ("work_tiles", ctypes.c_int64),
+        ("items", ctypes.c_int64),
+        ("partial_floats", ctypes.c_int64),
+        ("busiest_steps", ctypes.c_double),
+        ("efficiency", ctypes.c_double),
     ]
 
 
@@ -160,6 +179,8 @@ def load() -> ctypes.CDLL:
             lib.fs_ipc_free.restype = ctypes.c_int
             lib.fs_prepare.argtypes = [ctypes.POINTER(FsPrepParams), ctypes.c_void_p]
             lib.fs_prepare.restype = ctypes.c_int
+            lib.fs_plan.argtypes = [ctypes.POINTER(FsFwdParams), ctypes.c_int32, ctypes.POINTER(FsPlanInfo)]
+            lib.fs_plan.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -195,6 +216,14 @@ def load_torch_ext():
 
 def last_error() -> str:
     return load().fs_last_error().decode("utf-8", "replace")
+
+
+def plan(p: FsFwdParams, clusters: int = 0) -> FsPlanInfo:
+    """``fs_plan``: the split plan and wave-model efficiency of a launch (clusters > 0: host only)."""
+    info = FsPlanInfo()
+    if load().fs_plan(ctypes.byref(p), int(clusters), ctypes.byref(info)) != FS_OK:
+        raise ValueError(f"fs_plan: {last_error()}")
+    return info
 
 
 def query_tile(head_dim: int, dtype_code: int) -> tuple[int, int]:

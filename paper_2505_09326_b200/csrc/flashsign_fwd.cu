@@ -57,6 +57,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/flashsign.h"
 #include "sm100.cuh"
@@ -147,9 +148,14 @@ struct KParams {
   uint64_t* bad_key;
   // split K/V stream (streaming.py:122-128 merge): work tile = (batch, head, split, query block)
   int32_t n_batch;
-  int32_t kv_splits;       // >= 1
+  int32_t kv_splits;       // >= 1 (uniform mode: every work tile's K/V stream cut into this many ranges)
   int32_t split_tiles;     // K/V tiles per split (the last split may be shorter)
   int32_t n_kv_tiles;      // ceil(seqlen_kv / BN)
+  // tail mode (tail_splits > 0, kv_splits == 1): the work tiles [0, n_whole) fill whole waves of the
+  // persistent grid and run unsplit; the last partial wave's tail_T tiles are each cut into
+  // tail_splits K/V ranges (items n_whole + w * tail_splits + s), so the last wave keeps every
+  // cluster busy.  Their partials go to part_num / part_z, rows (s * tail_T + w) * TROWS + local.
+  int32_t tail_splits, n_whole, tail_T;
   float* part_num;         // non-NULL: write fp32 partial numerators [S][B][H][Nq][D] here instead of O
   float* part_z;           //           and partial z [S][B][H][Nq] (no normalisation, no bad-row check)
   // context parallelism over peer memory (fs_fwd_peer): partials go straight to the owner of
@@ -367,19 +373,36 @@ __device__ __forceinline__ void store32(typename OutT<OUT>::T* dst, const float*
   }
 }
 
+constexpr int TROWS = NQT * BM * CL;  // query rows of one cluster work tile
+
 struct TileCoord {
   int qblk, head, batch, split, kb0, L;  // K/V tiles [kb0, kb0 + L) of this work tile
+  bool part;                             // write fp32 partials (numerator, z) instead of O
+  int64_t pbase;                         // partial row of query position n = pbase + n
 };
 __device__ __forceinline__ TileCoord decode_tile(int tile, const KParams& p, int rank) {
   TileCoord c;
-  c.qblk = (tile % p.n_qblk) * CL + rank;  // the CTAs of a cluster take adjacent query blocks
-  const int rest = tile / p.n_qblk;
-  c.split = rest % p.kv_splits;
-  const int bh = rest / p.kv_splits;
+  const bool tail = p.tail_splits > 0 && tile >= p.n_whole;
+  int u = tile, w = 0, s = 0;  // u: the work tile in the unsplit order (tail mode)
+  if (tail) {
+    const int x = tile - p.n_whole;
+    w = x / p.tail_splits;
+    s = x - w * p.tail_splits;
+    u = p.n_whole + w;
+  }
+  const int qc = u % p.n_qblk;
+  c.qblk = qc * CL + rank;  // the CTAs of a cluster take adjacent query blocks
+  const int rest = u / p.n_qblk;
+  c.split = tail ? s : rest % p.kv_splits;
+  const int bh = tail ? rest : rest / p.kv_splits;
   c.head = bh % p.heads_q;
   c.batch = bh / p.heads_q;
+  const int span = (p.tail_splits > 0 && !tail) ? p.n_kv_tiles : p.split_tiles;
   c.kb0 = c.split * p.split_tiles;
-  c.L = min(p.split_tiles, p.n_kv_tiles - c.kb0);
+  c.L = min(span, p.n_kv_tiles - c.kb0);
+  c.part = tail || (p.tail_splits == 0 && p.part_num != nullptr);
+  c.pbase = tail ? (static_cast<int64_t>(s) * p.tail_T + w) * TROWS - static_cast<int64_t>(qc) * TROWS
+                 : ((static_cast<int64_t>(c.split) * p.n_batch + c.batch) * p.heads_q + c.head) * p.seqlen_q;
   return c;
 }
 
@@ -926,14 +949,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const int row = tc.qblk * (NQT * BM) + t * BM + r;
         const bool live = row < p.seqlen_q;
-        const bool partial = PEER || p.part_num != nullptr;
+        const bool partial = PEER || tc.part;
         const float zr = raw * fd.zrep;  // z in the reference's units (bad-row report, partials)
         const float den = NORM == FS_NORM_SIGNED_L1 ? raw + fd.eps_f : sqrtf(raw + fd.eps_f);
         // partial mode: the unnormalised numerator (the combine step divides by b(sum z + eps))
         float mul = partial ? fd.out_mul : __fdiv_rn(fd.out_sgn, den);
-        // partial row index: ((split * B + batch) * H + head) * Nq + row
-        const int64_t prow =
-            ((static_cast<int64_t>(tc.split) * p.n_batch + tc.batch) * p.heads_q + tc.head) * p.seqlen_q + row;
+        // partial row index: ((split * B + batch) * H + head) * Nq + row (tail mode: see KParams)
+        const int64_t prow = tc.pbase + row;
         // where this row's partial goes: the local workspace, or (peer mode) slot peer_rank of the
         // owner's workspace -- numerators [world][B][H][Rn][D] then z [world][B][H][Rn]
         float* num_dst = p.part_num + prow * D;
@@ -1208,35 +1230,176 @@ static int num_sms() {
   return cache[dev].load(std::memory_order_relaxed);
 }
 
-// K/V split plan: requested splits clamped to [1, n_kv_tiles], then every split non-empty.
+// Co-resident clusters of the persistent grid on the current device.  Every instantiation runs
+// one 768-thread CTA per SM with > 113 KB of dynamic shared memory in clusters of CL, so one
+// representative kernel answers for all (a GPC with an odd SM count holds one pair fewer).
+static int resident_clusters() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return std::max(1, num_sms() / CL);
+  static std::atomic<int> cache[kMaxDevices];
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n > 0) return n;
+  n = std::max(1, num_sms() / CL);
+  if constexpr (CL > 1) {
+    using C = Cfg<FS_BF16, 128, false>;
+    auto kern = flashsign_fwd_kernel<FS_BF16, 128, FS_BF16, FS_NORM_SPHERICAL, false, false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(n * CL);
+      cfg.blockDim = dim3(NUM_THREADS);
+      cfg.dynamicSmemBytes = C::SMEM_BYTES;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CL;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int m = 0;
+      if (cudaOccupancyMaxActiveClusters(&m, kern, &cfg) == cudaSuccess && m > 0) n = std::min(n, m);
+    }
+    cudaGetLastError();  // a failed query leaves no sticky error
+  }
+  cache[dev].store(n);
+  return n;
+}
+
+// K/V split plan.  Work tiles are (batch, head, 512-row query block) per cluster, walked by the G
+// co-resident clusters with a static stride.  Uniform mode cuts every work tile's K/V stream into
+// `splits` ranges (small B*H, long N); tail mode cuts only the tiles of the last, partial wave
+// (tiles = W*G + T, 0 < T < G), so that wave has T*splits items instead of T (e.g. 8-GPU shards
+// of C2 / C4: 256 tiles on 74 clusters = 3.46 waves -> 3 + 68/74).  Requested splits are clamped
+// to [1, K/V tiles] with every range non-empty.
 struct SplitPlan {
   int32_t splits, split_tiles, n_kv_tiles;
+  int32_t tail, n_whole, tail_T, clusters;
+  int64_t n_qblk, n_tiles0, n_items, part_rows;
 };
-static SplitPlan split_plan(const fs_fwd_params* p) {
-  SplitPlan sp;
+constexpr int kPlanOverhead = 2;  // per-item prologue + epilogue, in K/V-tile steps (wave model)
+
+// Wave-model choice of (splits, tail) for FS_SPLITS_AUTO.  Cost unit: one K/V-tile step of one
+// cluster work tile; each item pays kPlanOverhead; a split pays the combine pass (its partial
+// rows of Dk+1 fp32 read at ~5 TB/s, plus ~4 us of launch) converted into steps.
+static void auto_plan(const fs_fwd_params* p, const SplitPlan& sp, int G, int* s_out, bool* tail_out) {
+  *s_out = 1;
+  *tail_out = false;
+  const int64_t L = sp.n_kv_tiles, tiles = sp.n_tiles0;
+  if (tiles == 0 || L < 8) return;
+  const int dk = kernel_d(p);
+  const double step_s = 4.0 * (NQT * BM) * kernel_bn(p) * dk / 10.8e12;  // one CTA of the pair
+  const double rows = static_cast<double>(p->batch) * p->heads_q * p->seqlen_q;
+  auto comb = [&](double prow) { return (prow * (dk + 1) * 4.0 / 5.0e12 + 4.0e-6) / step_s; };
+  // costs of s = 1..smax; the smallest s within 0.5 % of the minimum wins (fewer Q reloads and
+  // partial rows than the model charges for)
+  const int64_t smax = std::min<int64_t>(16, L / 4);
+  double cost_of[17];
+  bool tail_of[17] = {};
+  std::fill(cost_of, cost_of + 17, 1e300);
+  cost_of[1] = static_cast<double>((tiles + G - 1) / G) * (L + kPlanOverhead);
+  tail_of[1] = false;
+  double best = cost_of[1];
+  const int64_t W = tiles / G, T = tiles % G;
+  for (int64_t s = 2; s <= smax; ++s) {
+    const int64_t st = (L + s - 1) / s, se = (L + st - 1) / st;
+    double cost;
+    bool tail;
+    if (tiles < G) {
+      cost = static_cast<double>((tiles * se + G - 1) / G) * (st + kPlanOverhead) + comb(se * rows);
+      tail = false;
+    } else {
+      if (T == 0) break;
+      cost = static_cast<double>(W) * (L + kPlanOverhead) +
+             static_cast<double>((T * se + G - 1) / G) * (st + kPlanOverhead) + comb(static_cast<double>(se * T * TROWS));
+      tail = true;
+    }
+    cost_of[s] = cost;
+    tail_of[s] = tail;
+    best = std::min(best, cost);
+  }
+  for (int64_t s = 1; s <= std::max<int64_t>(1, smax); ++s)
+    if (cost_of[s] <= best * 1.005) {
+      *s_out = static_cast<int>(s);
+      *tail_out = tail_of[s];
+      return;
+    }
+}
+
+// clusters: the co-resident cluster count to plan for (<= 0: query the current device)
+static SplitPlan split_plan(const fs_fwd_params* p, int clusters = 0) {
+  SplitPlan sp{};
   const int bn = kernel_bn(p);
   sp.n_kv_tiles = (p->seqlen_kv + bn - 1) / bn;
-  int s = std::max(1, p->kv_splits);
-  s = std::max(1, std::min(s, sp.n_kv_tiles));
+  sp.n_qblk = (static_cast<int64_t>(p->seqlen_q) + TROWS - 1) / TROWS;
+  sp.n_tiles0 = sp.n_qblk * p->heads_q * p->batch;
+  // context parallelism wants every row's partial: uniform mode only
+  const bool every_row = p->partial_only || g_peer != nullptr;
+  int s = p->kv_splits;
+  bool tail = p->split_tail != 0 && !every_row;
+  auto G = [&]() {
+    if (clusters <= 0) clusters = resident_clusters();
+    return clusters;
+  };
+  if (s == FS_SPLITS_AUTO) {
+    s = 1;
+    tail = false;
+    if (!every_row) auto_plan(p, sp, G(), &s, &tail);
+  }
+  s = std::max(1, std::min(std::max(1, s), sp.n_kv_tiles));
   sp.split_tiles = sp.n_kv_tiles > 0 ? (sp.n_kv_tiles + s - 1) / s : 0;
   sp.splits = sp.split_tiles > 0 ? (sp.n_kv_tiles + sp.split_tiles - 1) / sp.split_tiles : 1;
+  sp.clusters = clusters;
+  const int64_t rows = static_cast<int64_t>(p->batch) * p->heads_q * p->seqlen_q;
+  if (tail && sp.splits > 1) {
+    const int64_t g = G();
+    sp.clusters = clusters;
+    const int64_t T = sp.n_tiles0 % g;
+    if (T == 0) {  // whole waves: nothing to balance
+      sp.splits = 1;
+      sp.split_tiles = sp.n_kv_tiles;
+    } else {
+      sp.tail = 1;
+      sp.n_whole = static_cast<int32_t>(sp.n_tiles0 - T);
+      sp.tail_T = static_cast<int32_t>(T);
+    }
+  }
+  if (sp.tail) {
+    sp.n_items = sp.n_whole + static_cast<int64_t>(sp.tail_T) * sp.splits;
+    sp.part_rows = static_cast<int64_t>(sp.splits) * sp.tail_T * TROWS;
+  } else {
+    sp.n_items = sp.n_tiles0 * sp.splits;
+    sp.part_rows = sp.splits * rows;
+  }
   return sp;
 }
 
-
 // Merge of K/V-range partials (streaming.py:122-128, Lemma 1: (o, z) add, no
 // rescale): O = sum_s num_s / b(sum_s z_s + eps), plus the bad-row key.  One thread per 4 columns.
-template <int OUT, int NORM, int DK>
+// `rows` partial rows per part.  Uniform splits: partial row = (b*H + h)*Nq + n.  Tail splits
+// (TAIL): partial row = w*TROWS + local for tail work tile w, i.e. work tile u = n_whole + w of the
+// unsplit order, query position n = (u % n_qblk)*TROWS + local of (b, h) = u / n_qblk.
+template <int OUT, int NORM, int DK, bool TAIL>
 __global__ void __launch_bounds__(256) flashsign_combine_kernel(const float* __restrict__ num,
                                                                 const float* __restrict__ zp, int n_parts,
                                                                 int64_t rows, int heads, int seqlen_q, void* o,
                                                                 int64_t o_sb, int64_t o_sn, int64_t o_sh,
-                                                                int head_dim, float eps, uint64_t* bad_key) {
+                                                                int head_dim, float eps, uint64_t* bad_key,
+                                                                int n_whole, int n_qblk) {
   constexpr int TPR = DK / 4;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t row = gid / TPR;
   const int c4 = static_cast<int>(gid % TPR) * 4;
   if (row >= rows) return;
+  int n;
+  int64_t bh;
+  if constexpr (TAIL) {
+    const int64_t u = n_whole + row / TROWS;
+    n = static_cast<int>((u % n_qblk) * TROWS + row % TROWS);
+    bh = u / n_qblk;
+    if (n >= seqlen_q) return;  // past the sequence end: never written by the forward kernel
+  } else {
+    n = static_cast<int>(row % seqlen_q);
+    bh = row / seqlen_q;
+  }
   float z = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = 0; s < n_parts; ++s) {
@@ -1248,13 +1411,13 @@ __global__ void __launch_bounds__(256) flashsign_combine_kernel(const float* __r
     acc.w += a.w;
   }
   const float den = NORM == FS_NORM_SIGNED_L1 ? z + eps : sqrtf(z + eps);
-  if ((!(den > 0.f) || isinf(den)) && c4 == 0 && bad_key != nullptr)
+  if ((!(den > 0.f) || isinf(den)) && c4 == 0 && bad_key != nullptr) {
+    const uint64_t lin = static_cast<uint64_t>(bh) * seqlen_q + n;
     atomicMin(reinterpret_cast<unsigned long long*>(bad_key),
-              static_cast<unsigned long long>((static_cast<uint64_t>(row) << 32) | __float_as_uint(z)));
+              static_cast<unsigned long long>((lin << 32) | __float_as_uint(z)));
+  }
   if (c4 >= head_dim) return;
   const float inv = __fdiv_rn(1.0f, den);
-  const int n = static_cast<int>(row % seqlen_q);
-  const int64_t bh = row / seqlen_q;
   const int h = static_cast<int>(bh % heads);
   const int64_t b = bh / heads;
   using OT = typename OutT<OUT>::T;
@@ -1270,9 +1433,12 @@ __global__ void __launch_bounds__(256) flashsign_combine_kernel(const float* __r
   }
 }
 
+// rows / n_whole / n_qblk: see flashsign_combine_kernel (tail = 0: uniform splits, every row)
 template <int DK>
-static fs_status combine(const fs_fwd_params* p, int n_parts, cudaStream_t stream) {
-  const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
+static fs_status combine(const fs_fwd_params* p, int n_parts, cudaStream_t stream, int64_t tail_rows = 0,
+                         int n_whole = 0, int n_qblk = 1) {
+  const bool tail = tail_rows > 0;
+  const int64_t rows = tail ? tail_rows : (int64_t)p->batch * p->heads_q * p->seqlen_q;
   if (rows == 0) return FS_OK;
   const float* num = p->partial;
   const float* zp = p->partial + (int64_t)n_parts * rows * DK;
@@ -1280,25 +1446,29 @@ static fs_status combine(const fs_fwd_params* p, int n_parts, cudaStream_t strea
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   auto go = [&](auto kern) {
     kern<<<blocks, 256, 0, stream>>>(num, zp, n_parts, rows, p->heads_q, p->seqlen_q, p->o, p->o_stride[0],
-                                     p->o_stride[1], p->o_stride[2], p->head_dim, p->eps, p->bad_key);
+                                     p->o_stride[1], p->o_stride[2], p->head_dim, p->eps, p->bad_key, n_whole,
+                                     n_qblk);
   };
   const bool l1 = p->normalizer == FS_NORM_SIGNED_L1;
+#define FS_COMBINE_GO(OUT)                                                                           \
+  (tail ? (l1 ? go(flashsign_combine_kernel<OUT, FS_NORM_SIGNED_L1, DK, true>)                        \
+              : go(flashsign_combine_kernel<OUT, FS_NORM_SPHERICAL, DK, true>))                       \
+        : (l1 ? go(flashsign_combine_kernel<OUT, FS_NORM_SIGNED_L1, DK, false>)                       \
+              : go(flashsign_combine_kernel<OUT, FS_NORM_SPHERICAL, DK, false>)))
   switch (p->out_dtype) {
     case FS_F32:
-      l1 ? go(flashsign_combine_kernel<FS_F32, FS_NORM_SIGNED_L1, DK>)
-         : go(flashsign_combine_kernel<FS_F32, FS_NORM_SPHERICAL, DK>);
+      FS_COMBINE_GO(FS_F32);
       break;
     case FS_BF16:
-      l1 ? go(flashsign_combine_kernel<FS_BF16, FS_NORM_SIGNED_L1, DK>)
-         : go(flashsign_combine_kernel<FS_BF16, FS_NORM_SPHERICAL, DK>);
+      FS_COMBINE_GO(FS_BF16);
       break;
     case FS_F16:
-      l1 ? go(flashsign_combine_kernel<FS_F16, FS_NORM_SIGNED_L1, DK>)
-         : go(flashsign_combine_kernel<FS_F16, FS_NORM_SPHERICAL, DK>);
+      FS_COMBINE_GO(FS_F16);
       break;
     default:
       return fail(FS_ERR_DTYPE, "out_dtype must be FS_F32, FS_BF16 or FS_F16");
   }
+#undef FS_COMBINE_GO
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("combine launch: ") + cudaGetErrorString(e));
   return FS_OK;
@@ -1443,19 +1613,20 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   kp.dev_scales = p->dev_scales;
   kp.bad_key = p->bad_key;
   const SplitPlan sp = split_plan(p);
-  const int64_t n_qblk = (p->seqlen_q + NQT * BM * CL - 1) / (NQT * BM * CL);  // per cluster
-  const int64_t n_tiles = n_qblk * sp.splits * p->heads_q * p->batch;
+  const int64_t n_tiles = sp.n_items;
   if (n_tiles > INT32_MAX) return fail(FS_ERR_UNSUPPORTED, "too many work tiles for one launch");
-  kp.n_qblk = (int32_t)n_qblk;
+  kp.n_qblk = (int32_t)sp.n_qblk;
   kp.n_tiles = (int32_t)n_tiles;
   kp.n_batch = p->batch;
-  kp.kv_splits = sp.splits;
+  kp.kv_splits = sp.tail ? 1 : sp.splits;
   kp.split_tiles = sp.split_tiles;
   kp.n_kv_tiles = sp.n_kv_tiles;
+  kp.tail_splits = sp.tail ? sp.splits : 0;
+  kp.n_whole = sp.n_whole;
+  kp.tail_T = sp.tail_T;
   const bool partial = sp.splits > 1 || p->partial_only;
-  const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
   kp.part_num = partial ? p->partial : nullptr;
-  kp.part_z = partial ? p->partial + (int64_t)sp.splits * rows * D : nullptr;
+  kp.part_z = partial ? p->partial + sp.part_rows * D : nullptr;
   kp.peer = nullptr;
   kp.peer_world = kp.peer_rank = kp.peer_rows = 0;
   if (g_peer != nullptr) {
@@ -1498,7 +1669,10 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
-  if (sp.splits > 1 && !p->partial_only) return combine<D>(p, sp.splits, stream);
+  if (sp.splits > 1 && !p->partial_only)
+    return sp.tail ? combine<D>(p, sp.splits, stream, static_cast<int64_t>(sp.tail_T) * TROWS, sp.n_whole,
+                                static_cast<int>(sp.n_qblk))
+                   : combine<D>(p, sp.splits, stream);
   return FS_OK;
 }
 
@@ -1563,8 +1737,56 @@ int32_t fs_kv_splits(const fs_fwd_params* p) { return p ? fs::split_plan(p).spli
 
 int64_t fs_partial_floats(const fs_fwd_params* p) {
   if (!p) return 0;
-  const int64_t rows = (int64_t)p->batch * p->heads_q * p->seqlen_q;
-  return (int64_t)fs::split_plan(p).splits * rows * (fs::kernel_d(p) + 1);
+  return fs::split_plan(p).part_rows * (fs::kernel_d(p) + 1);
+}
+
+fs_status fs_plan(const fs_fwd_params* p, int32_t clusters, fs_plan_info* out) {
+  using namespace fs;
+  if (!p || !out) return fail(FS_ERR_CONFIG, "fs_plan: null argument");
+  if (p->kv_splits < FS_SPLITS_AUTO) return fail(FS_ERR_CONFIG, "kv_splits must be >= 0 or FS_SPLITS_AUTO");
+  if (p->batch < 0 || p->heads_q < 1 || p->seqlen_q < 0 || p->seqlen_kv < 0 || p->head_dim < 1)
+    return fail(FS_ERR_SHAPE, "fs_plan: bad extents");
+  if (clusters <= 0) clusters = resident_clusters();
+  const SplitPlan sp = split_plan(p, clusters);
+  std::memset(out, 0, sizeof(*out));
+  out->splits = sp.splits;
+  out->split_tail = sp.tail;
+  out->clusters = clusters;
+  out->n_whole = sp.n_whole;
+  out->tail_tiles = sp.tail_T;
+  out->n_kv_tiles = sp.n_kv_tiles;
+  out->work_tiles = sp.n_tiles0;
+  out->items = sp.n_items;
+  out->partial_floats = sp.part_rows * (kernel_d(p) + 1);
+  // static-stride assignment of the items to G clusters: K/V steps on the busiest cluster and
+  // the busy fraction (total steps / (G * busiest)).  Item i goes to cluster i % G.
+  const int64_t G = out->clusters > 0 ? out->clusters : 1;
+  auto item_len = [&](int64_t i) -> int64_t {
+    int64_t split = 0;
+    if (sp.tail) {
+      if (i < sp.n_whole) return sp.n_kv_tiles;
+      split = (i - sp.n_whole) % sp.splits;
+    } else {
+      split = (i / sp.n_qblk) % sp.splits;
+    }
+    return std::max<int64_t>(0, std::min<int64_t>(sp.split_tiles, sp.n_kv_tiles - split * sp.split_tiles));
+  };
+  const int64_t g_used = std::min<int64_t>(G, std::max<int64_t>(1, sp.n_items));
+  int64_t busiest = 0, total = 0;
+  if (sp.n_items <= (int64_t{1} << 22)) {
+    std::vector<int64_t> load(static_cast<size_t>(g_used), 0);
+    for (int64_t i = 0; i < sp.n_items; ++i) load[static_cast<size_t>(i % g_used)] += item_len(i);
+    for (int64_t v : load) {
+      busiest = std::max(busiest, v);
+      total += v;
+    }
+  } else {  // closed form for huge launches (uniform length items)
+    total = sp.n_items * item_len(0);
+    busiest = ((sp.n_items + g_used - 1) / g_used) * item_len(0);
+  }
+  out->busiest_steps = static_cast<double>(busiest);
+  out->efficiency = busiest > 0 ? static_cast<double>(total) / (static_cast<double>(G) * busiest) : 1.0;
+  return FS_OK;
 }
 
 fs_status fs_combine(const fs_fwd_params* p, int32_t n_parts, fs_stream_t stream_) {
@@ -1710,7 +1932,8 @@ fs_status fs_fwd(const fs_fwd_params* p, fs_stream_t stream_) {
     if (p->batch > 1 && (p->key_scale_stride < p->seqlen_kv || (p->key_scale_stride * 4) % 16 != 0))
       return fail(FS_ERR_UNSUPPORTED, "key_scale_stride must be >= seqlen_kv and a multiple of 4 elements");
   }
-  if (p->kv_splits < 0) return fail(FS_ERR_CONFIG, "kv_splits must be >= 0");
+  if (p->kv_splits < FS_SPLITS_AUTO) return fail(FS_ERR_CONFIG, "kv_splits must be >= 0 or FS_SPLITS_AUTO");
+  if (p->split_tail != 0 && p->split_tail != 1) return fail(FS_ERR_CONFIG, "split_tail must be 0 or 1");
   if (g_peer == nullptr && (split_plan(p).splits > 1 || p->partial_only) &&
       (p->partial == nullptr || !aligned16(p->partial)))
     return fail(FS_ERR_CONFIG, "kv_splits > 1 / partial_only need a 16-byte aligned `partial` workspace of "

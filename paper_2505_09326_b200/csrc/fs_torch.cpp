@@ -44,42 +44,6 @@ struct Fail {
   std::string msg;
 };
 
-int sm_count(int dev) {
-  static std::mutex mu;
-  static int cache[64] = {0};
-  std::lock_guard<std::mutex> g(mu);
-  if (dev < 0 || dev >= 64) return at::cuda::getDeviceProperties(dev)->multiProcessorCount;
-  if (cache[dev] == 0) cache[dev] = at::cuda::getDeviceProperties(dev)->multiProcessorCount;
-  return cache[dev];
-}
-
-// K/V splits for launches whose (b, h, 256-row) work tiles cannot fill the GPU: the wave model of
-// flashsign.auto_splits (one unit = one K/V tile step of one work tile; +2 per work tile for its
-// prologue / epilogue; plus the combine pass reading S partial rows of d+1 fp32).
-int auto_splits(int64_t b, int64_t h, int64_t nq, int64_t nkv, int d, int sms) {
-  const int64_t tiles = ((nq + 255) / 256) * h * b;
-  const int64_t n_kv = (nkv + 127) / 128;
-  if (tiles == 0 || tiles >= sms || n_kv < 8) return 1;
-  const int dk = d > 64 ? 128 : 64;
-  const double step_s = 4.0 * 256 * 128 * dk / 8.0e12;
-  const double rows = static_cast<double>(b * h * nq);
-  int best = 1;
-  double best_cost = 1e300;
-  const int64_t smax = std::min<int64_t>(16, n_kv / 4);
-  for (int64_t s = 1; s <= smax; ++s) {
-    const int64_t split_tiles = (n_kv + s - 1) / s;
-    const int64_t s_eff = (n_kv + split_tiles - 1) / split_tiles;
-    const int64_t waves = (tiles * s_eff + sms - 1) / sms;
-    const double comb = s_eff == 1 ? 0.0 : s_eff * rows * (dk + 1) * 4 / 5.0e12 / step_s;
-    const double cost = static_cast<double>(waves * (split_tiles + 2)) + comb;
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = static_cast<int>(s);
-    }
-  }
-  return best;
-}
-
 void check_bshd(const at::Tensor& t, const char* name) {
   if (!t.is_cuda()) throw Fail{FS_ERR_CUDA, std::string("flashsign: ") + name + " must be a CUDA tensor (no CPU fallback)"};
   if (t.dim() != 4) throw Fail{FS_ERR_SHAPE, std::string("flashsign: ") + name + " must be BSHD rank-4"};
@@ -91,7 +55,8 @@ py::tuple fwd(const at::Tensor& q, const at::Tensor& k, const at::Tensor& v, c10
               c10::optional<at::ScalarType> out_dtype, c10::optional<at::Tensor> bad_key, double scale, double eps,
               double p_scale, double q_descale, double k_descale, double v_descale, int64_t normalizer,
               c10::optional<at::Tensor> key_scale, int64_t kv_splits, c10::optional<at::Tensor> partial,
-              bool partial_only, c10::optional<at::Tensor> dev_scales, int64_t tile_m, int64_t tile_n) {
+              bool partial_only, c10::optional<at::Tensor> dev_scales, int64_t tile_m, int64_t tile_n,
+              bool split_tail) {
   try {
     check_bshd(q, "q");
     check_bshd(k, "k");
@@ -181,8 +146,9 @@ py::tuple fwd(const at::Tensor& q, const at::Tensor& k, const at::Tensor& v, c10
       p.key_scale = ks.data_ptr<float>();
       p.key_scale_stride = ks.stride(0);
     }
-    p.kv_splits = static_cast<int32_t>(
-        kv_splits >= 0 ? kv_splits : auto_splits(b, h, nq, nkv, static_cast<int>(d), sm_count(dev.index())));
+    // kv_splits < 0: the library's wave model picks the split (FS_SPLITS_AUTO, tail-only or uniform)
+    p.kv_splits = static_cast<int32_t>(kv_splits >= 0 ? kv_splits : FS_SPLITS_AUTO);
+    p.split_tail = split_tail ? 1 : 0;
     p.partial_only = partial_only ? 1 : 0;
     if (dev_scales.has_value()) {
       const at::Tensor& ds = *dev_scales;
@@ -221,6 +187,7 @@ PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
         py::arg("v"), py::arg("out"), py::arg("out_dtype"), py::arg("bad_key"), py::arg("scale"), py::arg("eps"),
         py::arg("p_scale"), py::arg("q_descale"), py::arg("k_descale"), py::arg("v_descale"),
         py::arg("normalizer"), py::arg("key_scale"), py::arg("kv_splits"), py::arg("partial"),
-        py::arg("partial_only"), py::arg("dev_scales"), py::arg("tile_m"), py::arg("tile_n"));
+        py::arg("partial_only"), py::arg("dev_scales"), py::arg("tile_m"), py::arg("tile_n"),
+        py::arg("split_tail"));
   m.def("version", []() { return fs_version(); });
 }

@@ -83,7 +83,7 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
               tile_hint: tuple[int, int] = (0, 0), normalizer: str = "spherical",
               key_scale: torch.Tensor | None = None, kv_splits: int | None = None,
               partial: torch.Tensor | None = None, partial_only: bool = False,
-              dev_scales: torch.Tensor | None = None):
+              dev_scales: torch.Tensor | None = None, split_tail: bool = False):
     """Launch FlashSign and return ``(o, bad_key)`` without synchronising.
 
     ``bad_key`` is a 1-element int64 CUDA tensor holding the packed first bad
@@ -91,9 +91,10 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
     ``key_scale`` (optional): float32 CUDA tensor ``[B, Nkv]`` (or ``[Nkv]`` when
     B == 1) of per-key multiplicities, finite and >= 0 -- not validated here
     (``fwd(check=True)`` does, like attention.py:386-387).
-    ``kv_splits``: K/V ranges per (b, h) (None: automatic -- split only when the
-    (b, h, 256-row) work tiles cannot fill the GPU); ranges merge by plain addition
-    of (numerator, z) (streaming.py:122-128), in a second small kernel.
+    ``kv_splits``: K/V ranges per (b, h) (None: automatic, see ``plan`` -- every work tile when the
+    (b, h, 512-row) tiles cannot fill the GPU, or only the last partial wave's tiles); ranges merge
+    by plain addition of (numerator, z) (streaming.py:122-128), in a second small kernel.
+    ``split_tail`` (with an explicit ``kv_splits``): split only the last partial wave's work tiles.
     With ``partial_only`` the call returns ``(partial, n_parts)`` instead (see ``fwd_partial``).
     ``dev_scales``: float32 CUDA tensor of 4 elements {q, k, v descale, p_scale} read by the kernel
     instead of the host values (written on the device, e.g. by ``prepare``; no host round trip).
@@ -106,7 +107,7 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
     args = (q, k, v, out, out_dtype, bad_key, float(scale), float(eps), float(p_scale), float(q_descale),
             float(k_descale), float(v_descale), NORMALIZERS[normalizer], key_scale,
             -1 if kv_splits is None else int(kv_splits), partial, bool(partial_only), dev_scales,
-            int(tile_hint[0]), int(tile_hint[1]))
+            int(tile_hint[0]), int(tile_hint[1]), bool(split_tail))
     global _ext
     ext = _ext or _lib.load_torch_ext()
     _ext = ext
@@ -122,36 +123,28 @@ def fwd_async(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float
     return o, bad
 
 
-_SMS: dict = {}
+def plan(b: int, h: int, nq: int, nkv: int, device, d: int = 128, dtype: torch.dtype = torch.bfloat16,
+         kv_splits: int | None = None, clusters: int = 0, split_tail: bool = False):
+    """The split plan ``fwd_async`` would use (C-ABI ``fs_plan``): ``kv_splits=None`` is the automatic
+    choice -- the library's wave model of the persistent grid splits the K/V stream of every work tile
+    when the (b, h, 512-row) tiles cannot fill the GPU (small batch, long sequence), or only the tiles
+    of the last, partial wave (``split_tail``) when a split there shortens the launch.  Returns the
+    ``fs_plan_info`` (splits, split_tail, efficiency, ...).  ``clusters`` > 0 plans for that many
+    co-resident 2-CTA clusters without touching a device."""
+    p = _lib.FsFwdParams()
+    p.batch, p.heads_q, p.heads_kv, p.seqlen_q, p.seqlen_kv, p.head_dim = b, h, h, nq, nkv, d
+    p.in_dtype = _IN_CODES[dtype]
+    p.kv_splits = _lib.FS_SPLITS_AUTO if kv_splits is None else int(kv_splits)
+    p.split_tail = int(bool(split_tail))
+    if clusters > 0:
+        return _lib.plan(p, clusters)
+    with torch.cuda.device(torch.device(device)):
+        return _lib.plan(p, 0)
 
 
 def auto_splits(b: int, h: int, nq: int, nkv: int, device, d: int = 128) -> int:
-    """K/V splits for launches whose (b, h, 256-row) work tiles cannot fill the GPU (small batch,
-    long sequence).  Picks S minimising a wave model, in units of one K/V-tile step of one work
-    tile (~2 us at d=128 on B200):  ceil(tiles*S / SMs) * (L/S + 2)  [2 = per-tile prologue and
-    epilogue]  +  the combine pass (S partial rows of d+1 fp32, read at ~5 TB/s).  1 when the
-    tiles already cover the SMs."""
-    dev = torch.device(device)
-    idx = dev.index if dev.index is not None else torch.cuda.current_device()
-    if idx not in _SMS:
-        _SMS[idx] = torch.cuda.get_device_properties(idx).multi_processor_count
-    sms = _SMS[idx]
-    tiles = -(-nq // 256) * h * b
-    n_kv = -(-nkv // 128)
-    if tiles == 0 or tiles >= sms or n_kv < 8:
-        return 1
-    dk = 128 if d > 64 else 64
-    step_s = 4.0 * 256 * 128 * dk / 8.0e12          # one K/V tile of one work tile on one SM
-    rows = b * h * nq
-
-    def cost(s_):
-        split_tiles = -(-n_kv // s_)
-        s_eff = -(-n_kv // split_tiles)
-        waves = -(-(tiles * s_eff) // sms)
-        comb = 0.0 if s_eff == 1 else s_eff * rows * (dk + 1) * 4 / 5.0e12 / step_s
-        return waves * (split_tiles + 2) + comb
-
-    return min(range(1, min(16, n_kv // 4) + 1), key=cost)
+    """K/V splits of the automatic plan (see ``plan``)."""
+    return plan(b, h, nq, nkv, device, d).splits
 
 
 def fwd_partial(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, **kw):
@@ -245,14 +238,14 @@ def fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float = 1.0
         out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None, p_scale: float = 1.0,
         q_descale: float = 1.0, k_descale: float = 1.0, v_descale: float = 1.0, check: bool = True,
         normalizer: str = "spherical", key_scale: torch.Tensor | None = None,
-        kv_splits: int | None = None) -> torch.Tensor:
+        kv_splits: int | None = None, split_tail: bool = False) -> torch.Tensor:
     """FlashSign forward ``O = c*sum_j s_ij v_j / sqrt(c^2 sum_j s_ij^2 + eps)`` on BSHD CUDA tensors
     (``normalizer="signed_l1"``: ``/ (|c| sum_j |s_ij| + eps)``)."""
     if check and key_scale is not None:
         check_key_scale(key_scale)
     o, bad = fwd_async(q, k, v, scale=scale, eps=eps, out=out, out_dtype=out_dtype, p_scale=p_scale,
                        q_descale=q_descale, k_descale=k_descale, v_descale=v_descale, normalizer=normalizer,
-                       key_scale=key_scale, kv_splits=kv_splits)
+                       key_scale=key_scale, kv_splits=kv_splits, split_tail=split_tail)
     if check:
         raise_if_bad(bad, q.shape[2], q.shape[1])
     return o

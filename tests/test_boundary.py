@@ -53,7 +53,8 @@ def test_library_is_sm100a_with_tcgen05():
 
 
 @pytest.mark.parametrize("cname,cls", [("fs_fwd_params", _lib.FsFwdParams), ("fs_peer_params", _lib.FsPeerParams),
-                                       ("fs_prep_tensor", _lib.FsPrepTensor), ("fs_prep_params", _lib.FsPrepParams)])
+                                       ("fs_prep_tensor", _lib.FsPrepTensor), ("fs_prep_params", _lib.FsPrepParams),
+                                       ("fs_plan_info", _lib.FsPlanInfo)])
 def test_struct_layout_matches_header(tmp_path, cname, cls):
     fields = [f[0] for f in cls._fields_]
     prog = tmp_path / "layout.c"
@@ -256,11 +257,40 @@ def test_split_plan_host_functions():
 
 
 def test_auto_splits_wave_model():
-    import paper_2505_09326_b200.flashsign as fsm
-    fsm._SMS[0] = 148
-    assert fsm.auto_splits(8, 16, 16384, 16384, "cuda:0", 128) == 1       # C3: 8192 tiles
-    assert fsm.auto_splits(1, 1, 16384, 16384, "cuda:0", 128) > 1         # 64 tiles on 148 SMs
-    assert fsm.auto_splits(1, 1, 300, 700, "cuda:0", 128) == 1            # too few K/V tiles (6)
+    # FS_SPLITS_AUTO planned for 74 co-resident clusters (148-SM B200), host only
+    def plan(b, h, n, d=128, dt=_lib.FS_BF16):
+        p = _params(head_dim=d, seqlen_kv=n, seqlen_q=n, batch=b, heads_q=h, heads_kv=h)
+        p.in_dtype = dt
+        p.kv_splits = _lib.FS_SPLITS_AUTO
+        return _lib.plan(p, 74)
+    assert plan(1, 1, 16384).splits > 1 and plan(1, 1, 16384).split_tail == 0   # 32 tiles: uniform split
+    assert plan(1, 1, 300, 128).splits == 1                                    # too few K/V tiles (3)
+    c3 = plan(8, 16, 16384)      # 4096 tiles = 55 waves + 26: the tail wave is split in two
+    assert (c3.splits, c3.split_tail, c3.n_whole, c3.tail_tiles) == (2, 1, 55 * 74, 26)
+    assert c3.items == 55 * 74 + 52 and c3.efficiency > 0.995
+    assert plan(16, 16, 4096, 64, _lib.FS_F16).splits == 1   # C2 on one GPU: 27.7 waves, a split would not pay
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_wave_efficiency_of_sharded_configs(world):
+    # batch x head shards of C2-C5 (BASELINE.json configs) on `world` GPUs: each rank's launch
+    # keeps >= 95 % of the persistent grid's clusters busy (static-stride wave model, 74 clusters)
+    from paper_2505_09326_b200 import partition
+    cfgs = {"c2": (16, 16, 4096, 64, _lib.FS_F16), "c3": (8, 16, 16384, 128, _lib.FS_BF16),
+            "c4": (8, 16, 8192, 128, _lib.FS_E4M3), "c5": (64, 8, 20000, 64, _lib.FS_BF16)}
+    for name, (b, h, n, d, dt) in cfgs.items():
+        for rank in range(world):
+            lo, hi = partition.unit_range(b * h, world, rank)
+            for pc in partition.pieces(b, h, lo, hi):
+                p = _params(head_dim=d, seqlen_kv=n, seqlen_q=n, batch=pc.b1 - pc.b0, heads_q=pc.g1 - pc.g0,
+                            heads_kv=pc.g1 - pc.g0)
+                p.in_dtype = dt
+                p.kv_splits = _lib.FS_SPLITS_AUTO
+                info = _lib.plan(p, 74)
+                assert info.efficiency >= 0.95, (name, world, rank, info.splits, info.split_tail, info.efficiency)
+                p.kv_splits = 1
+                unsplit = _lib.plan(p, 74).efficiency
+                assert info.efficiency >= unsplit - 1e-9
 
 
 def test_integration_c_snippet_compiles(tmp_path):
