@@ -122,6 +122,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_P2_NQB2
 #define FS_P2_NQB2 0  // CTA pairs at d=128: double-buffer Q (fewer ring slots)
 #endif
+#ifndef FS_DEFER_Z
+#define FS_DEFER_Z 1  // 16-bit inputs: the norm warps' last-chunk a2(s) accumulation after the P hand-off
+#endif
 #ifndef FS_P2_STAGES
 #define FS_P2_STAGES 0  // CTA-pair ring depth override (0: as many half-tile slots as fit)
 #endif
@@ -811,6 +814,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // BN/2 columns in 32-column chunks (80 registers/thread at 768 threads): the next chunk's
         // TMEM load is issued once this chunk is packed, and overlaps this chunk's P store.
         constexpr int NCH = BN / 64;
+        // 16-bit P, 192-key tiles: accumulate the last chunk's a2(s) after the P hand-off (FP8: the e4m3 conversion
+        // runs on its own pipe and hides the FFMA2s; its saturation check needs the sums first)
+        constexpr bool DEFER_Z = FS_DEFER_Z && !TR::F8 && NCH >= 3;
         uint32_t s[32];
         ptx::tmem_ld32(s_addr, s);
         ptx::tmem_wait_ld();
@@ -819,6 +825,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t pk8[TR::SAT_CHECK ? NCH * 8 : 1];
         // sum of a2(s) over this half: packed FP32 FMAs / adds, two independent chains
         float2 h0 = make_float2(0.f, 0.f), h1 = h0;
+        auto accum_a2 = [&](float2 a, float2 b) {
+          if constexpr (NORM == FS_NORM_SIGNED_L1) {
+            h0 = __fadd2_rn(h0, make_float2(fabsf(a.x), fabsf(a.y)));
+            h1 = __fadd2_rn(h1, make_float2(fabsf(b.x), fabsf(b.y)));
+          } else {
+            h0 = __ffma2_rn(a, a, h0);
+            h1 = __ffma2_rn(b, b, h1);
+          }
+        };
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
           // (a2(s) accumulates into the half's h0 / h1 chains)  With KS the scores are
@@ -838,13 +853,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               s[i + 2] = __float_as_uint(b.x);
               s[i + 3] = __float_as_uint(b.y);
             }
-            if constexpr (NORM == FS_NORM_SIGNED_L1) {
-              h0 = __fadd2_rn(h0, make_float2(fabsf(a.x), fabsf(a.y)));
-              h1 = __fadd2_rn(h1, make_float2(fabsf(b.x), fabsf(b.y)));
-            } else {
-              h0 = __ffma2_rn(a, a, h0);
-              h1 = __ffma2_rn(b, b, h1);
-            }
+            if (!(DEFER_Z && ch == NCH - 1)) accum_a2(a, b);
           }
           // pack P (s[i] is written only after s[2i], s[2i+1] / s[4i..4i+3] are read)
           uint32_t pk_local[16];
@@ -876,8 +885,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tmem_st16(s_addr + ch * 16, pk);
           if (ch + 1 < NCH) ptx::tmem_wait_ld();
         }
-        za = __fadd2_rn(za, h0);
-        zb = __fadd2_rn(zb, h1);
+        if constexpr (!DEFER_Z) {
+          za = __fadd2_rn(za, h0);
+          zb = __fadd2_rn(zb, h1);
+        }
         if constexpr (TR::SAT_CHECK) {
           // max|s| <= sqrt(sum s^2) (<= sum |s|): only a half whose sum reaches ovf_z can hold a
           // saturated code; then look for 0x7e / 0xfe (+-448) in its packed P
@@ -899,6 +910,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_arrive_cluster(lead(&bars->p_full[sb]));  // the pair leader issues PV
           else
             ptx::mbar_arrive(&bars->p_full[sb]);
+        }
+        if constexpr (DEFER_Z) {
+          // the last chunk's a2(s) after P is handed over: off the P critical path (16-bit P: the
+          // FFMA2s share the conversion's pipe); s still holds that chunk
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            accum_a2(make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1])),
+                     make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
+          za = __fadd2_rn(za, h0);
+          zb = __fadd2_rn(zb, h1);
         }
 #if FS_PROF
         pr_nc += clock64() - tn1;
@@ -994,6 +1015,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
+          if (c == 0) {
+            // FP16 P overflow: an inf P_ij makes EVERY column of O_i non-finite (inf * v, or
+            // inf * 0 = NaN) and needs raw z >= (65504/p)^2.  Only rows past that z bound are
+            // scanned, before the first accumulator chunk is loaded (so no register set is live
+            // besides the scan's): no finite column = overflow.  A NaN / inf in V alone (some
+            // columns) is passed through unflagged, as the reference does.
+            bool ovf_row = false;
+            if constexpr (TR::INF_CHECK) {
+              const bool cand = tc.L > 0 && isfinite(raw) && raw >= ovf_raw;
+              if (__any_sync(0xffffffffu, cand)) {  // warp-uniform: tcgen05.ld is warp-collective
+                bool fin = false;
+#pragma unroll 1
+                for (int c2 = 0; c2 < D / 32; ++c2) {
+                  uint32_t w[32];
+                  ptx::tmem_ld32(o_addr + c2 * 32, w);
+                  ptx::tmem_wait_ld();
+#pragma unroll
+                  for (int i = 0; i < 32; ++i)
+                    if (c2 * 32 + i < p.head_dim && isfinite(__uint_as_float(w[i]))) fin = true;
+                }
+                ovf_row = cand && !fin;
+              }
+            }
+            finish_row(ovf_row);
+          }
           uint32_t acc[32];
           float v[32];
           if (tc.L > 0) {
@@ -1012,32 +1058,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] = 0u;
-          }
-          if (c == 0) {
-            // FP16 P overflow: an inf P_ij makes EVERY column of O_i non-finite (inf * v, or
-            // inf * 0 = NaN) and needs raw z >= (65504/p)^2.  Rows passing both cheap tests (column
-            // 0 non-finite, z in range) are confirmed by scanning all columns, so a NaN / inf in
-            // V alone (some columns) is passed through unflagged, as the reference does.
-            bool suspect = false;
-            if constexpr (TR::INF_CHECK) {
-              const float a0 = __uint_as_float(acc[0]);
-              suspect = tc.L > 0 && !isfinite(a0) && isfinite(raw) && raw >= ovf_raw;
-              if (__any_sync(0xffffffffu, suspect)) {  // warp-uniform: tcgen05.ld is warp-collective
-                uint32_t w[32];
-#pragma unroll 1
-                for (int c2 = 0; c2 < D / 32; ++c2) {
-                  if (c2 > 0) {
-                    ptx::tmem_ld32(o_addr + c2 * 32, w);
-                    ptx::tmem_wait_ld();
-                  }
-                  const uint32_t* src = c2 == 0 ? acc : w;
-#pragma unroll
-                  for (int i = 0; i < 32; ++i)
-                    if (c2 * 32 + i < p.head_dim && isfinite(__uint_as_float(src[i]))) suspect = false;
-                }
-              }
-            }
-            finish_row(suspect);
           }
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = (mul == 0.f) ? 0.f : __uint_as_float(acc[i]) * mul;

@@ -1,0 +1,118 @@
+// ALU throughput microbenchmark (experiment, not product): the per-score instructions of the
+// FlashSign norm step -- fp32 -> fp16x2 / bf16x2 / e4m3x2 conversion (F2FP), packed FFMA2 --
+// issued by W warps per SM sub-partition, 16 independent chains per thread.  Prints cycles per
+// warp instruction per sub-partition (1.0 = one warp instruction per clock).
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <cstdio>
+#include <cstdint>
+
+constexpr int CH = 16;
+
+template <int OP>
+__device__ __forceinline__ void step(float (&f)[CH], uint32_t (&u)[CH]) {
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    if constexpr (OP == 0) {  // cvt.rn.f16x2.f32
+      asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(f[i]), "f"(__uint_as_float(u[i])));
+    } else if constexpr (OP == 1) {  // cvt.rn.bf16x2.f32
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(f[i]), "f"(__uint_as_float(u[i])));
+    } else if constexpr (OP == 2) {  // cvt e4m3x2 (16-bit result)
+      uint16_t h;
+      asm volatile("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(f[i]), "f"(__uint_as_float(u[i])));
+      u[i] = h;
+    } else if constexpr (OP == 3) {  // fma.rn.f32x2 (FFMA2)
+      uint64_t a = (uint64_t(u[i]) << 32) | __float_as_uint(f[i]);
+      asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(a));
+      u[i] = uint32_t(a >> 32);
+      f[i] = __uint_as_float(uint32_t(a));
+    } else if constexpr (OP == 4) {  // scalar FFMA
+      asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(f[i]));
+    } else if constexpr (OP == 5) {  // cvt.rn.f16x2.f32 + fma.rn.f32x2 interleaved (the norm mix)
+      uint64_t a = (uint64_t(u[i]) << 32) | __float_as_uint(f[i]);
+      asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(a));
+      uint32_t h;
+      asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(__uint_as_float(uint32_t(a))), "f"(__uint_as_float(uint32_t(a >> 32))));
+      u[i] = h ^ uint32_t(a >> 32);
+      f[i] = __uint_as_float(uint32_t(a));
+    } else if constexpr (OP == 7) {  // cvt f16x2 -> e4m3x2
+      uint16_t h;
+      asm volatile("cvt.rn.satfinite.e4m3x2.f16x2 %0, %1;" : "=h"(h) : "r"(u[i] ^ __float_as_uint(f[i])));
+      u[i] = h;
+    } else if constexpr (OP == 8) {  // PRMT (bf16 truncating pack of two fp32)
+      asm volatile("prmt.b32 %0, %1, %0, 0x7632;" : "+r"(u[i]) : "r"(__float_as_uint(f[i])));
+    } else if constexpr (OP == 9) {  // FFMA2 + PRMT interleaved
+      uint64_t a = (uint64_t(u[i]) << 32) | __float_as_uint(f[i]);
+      asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(a));
+      uint32_t h = uint32_t(a >> 32);
+      asm volatile("prmt.b32 %0, %1, %0, 0x7632;" : "+r"(h) : "r"(uint32_t(a)));
+      u[i] = h;
+      f[i] = __uint_as_float(uint32_t(a));
+    } else if constexpr (OP == 10) {  // FFMA2 + cvt.e4m3x2 interleaved (the FP8 norm mix, 1:1)
+      uint64_t a = (uint64_t(u[i]) << 32) | __float_as_uint(f[i]);
+      asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(a));
+      uint16_t h;
+      asm volatile("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(__uint_as_float(uint32_t(a))), "f"(__uint_as_float(uint32_t(a >> 32))));
+      u[i] = h ^ uint32_t(a >> 32);
+      f[i] = __uint_as_float(uint32_t(a));
+    } else if constexpr (OP == 11) {  // HFMA2 (f16x2)
+      asm volatile("fma.rn.f16x2 %0, %0, %0, %0;" : "+r"(u[i]));
+    } else if constexpr (OP == 12) {  // IADD3-like int add
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(u[i]) : "r"(__float_as_uint(f[i])));
+    } else if constexpr (OP == 6) {  // F2F half2 via two scalar cvt (cvt.rn.f16.f32 x2 + pack)
+      uint16_t lo, hi;
+      asm volatile("cvt.rn.f16.f32 %0, %1;" : "=h"(lo) : "f"(f[i]));
+      asm volatile("cvt.rn.f16.f32 %0, %1;" : "=h"(hi) : "f"(__uint_as_float(u[i])));
+      u[i] = (uint32_t(hi) << 16) | lo;
+    }
+  }
+}
+
+template <int OP>
+__global__ void bench(int iters, unsigned long long* out, float seed) {
+  float f[CH];
+  uint32_t u[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    f[i] = seed * (i + 1) * 1e-3f;
+    u[i] = __float_as_uint(seed * (i + 2) * 1e-3f);
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) step<OP>(f, u);
+  __syncthreads();
+  const long long t1 = clock64();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) acc ^= u[i] ^ __float_as_uint(f[i]);
+  if (acc == 0x12345678u) out[1] = acc;
+  if (threadIdx.x == 0) out[0] = t1 - t0;
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 16);
+  const char* names[] = {"cvt.f16x2", "cvt.bf16x2", "cvt.e4m3x2", "FFMA2", "FFMA", "FFMA2+cvt.f16x2", "2x cvt.f16",
+                         "cvt f16x2->e4m3x2", "PRMT", "FFMA2+PRMT", "FFMA2+cvt.e4m3x2", "HFMA2", "IADD"};
+  const int iters = 4096;
+  for (int op = 0; op < 13; ++op) {
+    for (int w : {2, 4}) {
+      const int threads = 128 * w;  // w warps per sub-partition
+      void (*k)(int, unsigned long long*, float) = nullptr;
+      switch (op) { case 0: k = bench<0>; break; case 1: k = bench<1>; break; case 2: k = bench<2>; break;
+        case 3: k = bench<3>; break; case 4: k = bench<4>; break; case 5: k = bench<5>; break; case 6: k = bench<6>; break;
+        case 7: k = bench<7>; break; case 8: k = bench<8>; break; case 9: k = bench<9>; break; case 10: k = bench<10>; break;
+        case 11: k = bench<11>; break; default: k = bench<12>; }
+      k<<<1, threads>>>(64, d, 1.0f);
+      k<<<1, threads>>>(iters, d, 1.0f);
+      unsigned long long cyc = 0;
+      cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+      const double instr_per_smsp = double(iters) * CH * w * (op == 5 || op == 6 || op == 9 || op == 10 ? 2 : 1);
+      printf("%-18s warps/SMSP %d: %.3f cycles per warp instr per SMSP\n", names[op], w, cyc / instr_per_smsp);
+    }
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("%s\n", cudaGetErrorString(e));
+  return 0;
+}
