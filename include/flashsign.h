@@ -217,6 +217,17 @@ typedef struct {
 
 fs_status fs_prepare(const fs_prep_params *p, fs_stream_t stream);
 
+/* K' = m K for 16-bit inputs: k_out[b, n, h, :] = RNE(key_scale[b*key_scale_stride + n] * k[b, n, h, :])
+   (fp32 product: exact for integer m), the reference's apply_multiplicity_array (attention.py:381-388,
+   grn.py:150) as one HBM-bound pass.  Uses p->k, k_stride, batch, seqlen_kv, heads_kv, head_dim (a
+   multiple of 8), in_dtype (FS_F16 | FS_BF16), key_scale, key_scale_stride; k_out strides in
+   elements, 16-byte multiples.  Then fs_fwd with k = k_out and key_scale = NULL computes the
+   multiplicity attention with the tensor cores' operand traffic unchanged: for 16-bit inputs this
+   is cheaper than fs_fwd's in-kernel key_scale (one extra multiply per score on the norm step's
+   critical path, measured -20 % at d = 64; scaling the K slot in shared memory instead exceeds the
+   SM's shared-memory bandwidth, FS_KS_SMEM).  Async on `stream`. */
+fs_status fs_scale_keys(const fs_fwd_params *p, void *k_out, const int64_t *k_out_stride, fs_stream_t stream);
+
 /* Thread-local text of the last non-FS_OK status. */
 const char *fs_last_error(void);
 

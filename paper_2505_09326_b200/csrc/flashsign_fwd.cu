@@ -57,6 +57,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/flashsign.h"
@@ -121,6 +122,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #endif
 #ifndef FS_P2_NQB2
 #define FS_P2_NQB2 0  // CTA pairs at d=128: double-buffer Q (fewer ring slots)
+#endif
+#ifndef FS_KS_SMEM
+#define FS_KS_SMEM 0  // experiment: 16-bit multiplicities scaled in the K slot in shared memory (Cfg::KSM)
 #endif
 #ifndef FS_DEFER_Z
 #define FS_DEFER_Z 1  // 16-bit inputs: the norm warps' last-chunk a2(s) accumulation after the P hand-off
@@ -247,6 +251,14 @@ struct Cfg {
   // of the columns (the MMA's B operand is split along N between the pair).  The multiplicity
   // variant (KS) keeps one MMA per CTA with multicast K/V.
   static constexpr bool P2 = FS_2SM && CL == 2 && !KS && (FS_2SM == 2 || (!TR::F8 && D == 128));
+  // Experiment (FS_KS_SMEM=1, 16-bit inputs with multiplicities): K_j' = m_j K_j formed in the K ring
+  // slot by the otherwise idle warps 2-3 (packed HMUL2, one rounding -- the numerics of pre-scaling
+  // K), once per CTA and K/V tile, instead of m_j s_ij per score in the norm step.  Measured equal at
+  // d=64 and -10 % at d=128: the slot's extra read + write (~32 B/clk) pushes the SM past its
+  // shared-memory bandwidth, which the SS MMAs already use at 83-128 B/clk.  The torch entry instead
+  // forms K' in one HBM pass (fs_scale_keys); FP8 keeps the per-score multiply (its norm step is
+  // bound by the e4m3 conversion pipe, where the FMUL2s hide).
+  static constexpr bool KSM = KS && !TR::F8 && FS_KS_SMEM;
   static constexpr int KROWS = P2 ? BN / 2 : BN;                   // K rows in a CTA's slot
   static constexpr int VROW_BYTES = P2 ? ROW_BYTES / 2 : ROW_BYTES;  // bytes per key in a CTA's V slot
   static constexpr int V_SW = (VROW_BYTES % 128 == 0) ? 128 : 64;  // V slot swizzle span (B)
@@ -305,6 +317,7 @@ struct Cfg {
 struct Bars {
   uint64_t q_full[NQT][2], q_empty[NQT][2];
   uint64_t kv_full[16], kv_empty[16];
+  uint64_t ks_full[16];     // Cfg::KSM: the K slot holds m_j K_j (warps 2 and 3 arrived)
   uint64_t s_full[2];       // per S buffer (= Q tile)
   uint64_t p_full[2];       // per S buffer: all norm warps of the tile (both CTAs of a pair) wrote P
   uint64_t o_full[NQT][2], o_empty[NQT][2];
@@ -454,6 +467,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
     for (int s = 0; s < C::STAGES; ++s) {
+      if (C::KSM) ptx::mbar_init(&bars->ks_full[s], 2);
       ptx::mbar_init(&bars->kv_full[s], 1);
       ptx::mbar_init(&bars->kv_empty[s], C::P2 ? 1 : CL);  // both CTAs' MMAs (multicast) / the pair MMA
     }
@@ -532,7 +546,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int i = 0; i < 2 * L; ++i, ++kv_i) {
           const uint32_t slot = kv_i % C::STAGES;
           const uint32_t round = kv_i / C::STAGES;
-          const bool with_m = KS && (i & 1);  // V slots also carry the tile's key multiplicities
+          // the tile's key multiplicities ride in the K slot (KSM: scaled into K) or the V slot (FP8:
+          // read by the norm warps)
+          const bool with_m = KS && (C::KSM ? !(i & 1) : (i & 1));
           uint64_t* full = &bars->kv_full[C::kv_bar(slot)];
           if (FS_TMA_ONCE && !C::P2 && kv_i >= C::STAGES) {  // experiment: no K/V traffic after the first ring
             if (!C::KV1 || !(i & 1)) {
@@ -548,7 +564,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // leader announces both CTAs' halves
             if (!C::P2 || rank == 0)
               ptx::mbar_arrive_expect_tx(full, (C::P2 ? 2 : 1) * (C::KV1 ? 2 : 1) * C::SLOT_BYTES +
-                                                   (KS ? C::MS_SLOT_BYTES : 0) * (C::KV1 ? 1 : (i & 1)));
+                                                   (KS ? C::MS_SLOT_BYTES : 0) * (C::KV1 || with_m ? 1 : 0));
           }
           const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
           const int key0 = (tc.kb0 + (i >> 1)) * BN;
@@ -717,6 +733,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const long long tk0 = clock64();
 #endif
           ptx::mbar_wait(&bars->kv_full[C::kv_bar(k_slot)], (k_idx / C::STAGES) & 1u);
+          if constexpr (C::KSM) ptx::mbar_wait(&bars->ks_full[k_slot], (k_idx / C::STAGES) & 1u);
 #if FS_PROF
           pr_kw += clock64() - tk0;
           ++pr_kn;
@@ -765,6 +782,74 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     FS_PROF_ADD(7, clock64() - pr_t0); }
 #endif
     }
+  } else if (C::KSM && (warp == 2 || warp == 3)) {
+    // ------------------------------------------------------------ K scaling (Cfg::KSM)
+    // K_j' = m_j K_j in the K ring slot, in place: a 16-byte chunk holds 8 elements of one key row
+    // (the 128B swizzle permutes chunks within a row), so chunk x scales by m of row
+    // (x mod BN*8) / 8.  Integer (any 16-bit-representable) m: packed HMUL2, one rounding, exactly
+    // what pre-scaling K in float64 and casting gives; other m: fp32 multiply, then RNE.
+    using E2 = typename std::conditional<IN == FS_BF16, __nv_bfloat162, __half2>::type;
+    uint32_t kv_i = 0;
+    for (int tile = tile0; tile < p.n_tiles && n_kv_tiles > 0; tile += tstride) {
+      const int L = decode_tile(tile, p, rank).L;
+      for (int j = 0; j < L; ++j, kv_i += 2) {
+        const uint32_t slot = kv_i % C::STAGES;
+        ptx::mbar_wait(&bars->kv_full[C::kv_bar(slot)], (kv_i / C::STAGES) & 1u);
+        const float* ms = reinterpret_cast<const float*>(smem + C::MS_OFF + slot * C::MS_SLOT_BYTES);
+        uint4* base = reinterpret_cast<uint4*>(smem + C::RING_OFF + slot * C::SLOT_BYTES);
+        // 8 chunks per thread in flight: loads first, then the multiplies, then the stores (one
+        // chunk at a time would serialise on the shared-memory latency)
+        constexpr int CPT = C::SLOT_BYTES / 16 / 64, NBT = 8;
+        static_assert(CPT % NBT == 0, "K slot chunks per scaler thread");
+#pragma unroll 1
+        for (int b0 = 0; b0 < CPT; b0 += NBT) {
+          uint4 w[NBT];
+          float m[NBT];
+          bool exact = true;
+#pragma unroll
+          for (int u = 0; u < NBT; ++u) {
+            const int x = (b0 + u) * 64 + (warp - 2) * 32 + lane;
+            w[u] = base[x];
+            m[u] = ms[(x % (BN * 8)) / 8];
+          }
+#pragma unroll
+          for (int u = 0; u < NBT; ++u) {
+            E2 m2;
+            if constexpr (IN == FS_BF16) m2 = __float2bfloat162_rn(m[u]);
+            else m2 = __float2half2_rn(m[u]);
+            exact = exact && (__low2float(m2) == m[u]);
+          }
+          if (__all_sync(0xffffffffu, exact)) {
+#pragma unroll
+            for (int u = 0; u < NBT; ++u) {
+              E2 m2;
+              if constexpr (IN == FS_BF16) m2 = __float2bfloat162_rn(m[u]);
+              else m2 = __float2half2_rn(m[u]);
+              E2* e = reinterpret_cast<E2*>(&w[u]);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) e[k] = __hmul2(e[k], m2);
+            }
+          } else {  // fp32 product then RNE (bitwise the same as HMUL2 when m is representable)
+#pragma unroll
+            for (int u = 0; u < NBT; ++u) {
+              E2* e = reinterpret_cast<E2*>(&w[u]);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                float2 f2;
+                if constexpr (IN == FS_BF16) f2 = __bfloat1622float2(e[k]);
+                else f2 = __half22float2(e[k]);
+                reinterpret_cast<uint32_t*>(&w[u])[k] = pack2<IN>(f2.x * m[u], f2.y * m[u]);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < NBT; ++u) base[(b0 + u) * 64 + (warp - 2) * 32 + lane] = w[u];
+        }
+        ptx::fence_proxy_async();  // generic-proxy stores -> visible to the tensor core's reads
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&bars->ks_full[slot]);
+      }
+    }
   } else if (warp >= WARP_NORM0 && warp < WARP_EPI) {
     // ------------------------------------------------------------ norm warps
     // Eight warps per Q tile: warp (t, h, quarter) owns TMEM lanes 32*quarter.. and the
@@ -800,7 +885,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // key multiplicities of this K/V tile ride in V_j's ring slot; that slot is released only
         // after PV_1(j), which needs this warp's P, so they stay valid while they are read here
         const uint32_t v_idx = 2u * s_use + 1u, v_slot = v_idx % C::STAGES;
-        if constexpr (KS) ptx::mbar_wait(&bars->kv_full[C::kv_bar(v_slot)], (v_idx / C::STAGES) & 1u);
+        if constexpr (KS && !C::KSM) ptx::mbar_wait(&bars->kv_full[C::kv_bar(v_slot)], (v_idx / C::STAGES) & 1u);
         ++s_use;
 #if FS_PROF
         const long long tn1 = clock64();
@@ -844,7 +929,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int i = 0; i < 32; i += 4) {
             float2 a = make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1]));
             float2 b = make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
-            if constexpr (KS) {
+            if constexpr (KS && !C::KSM) {
               const float4 m4 = mp[i / 4];
               a = __fmul2_rn(a, make_float2(m4.x, m4.y));
               b = __fmul2_rn(b, make_float2(m4.z, m4.w));

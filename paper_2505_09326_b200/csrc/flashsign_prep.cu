@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "../../include/flashsign.h"
 
@@ -220,6 +221,44 @@ __global__ void __launch_bounds__(kThreads) quant_kernel(PrepArgs p) {
   }
 }
 
+// ------------------------------------------------------------------ K' = m K (fs_scale_keys)
+// One 16-byte chunk (8 elements of one key row) per thread and step: read, multiply in fp32 (exact
+// for integer m and 16-bit K), round to nearest even, write.  HBM-bound streaming pass.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) scale_keys_kernel(const T* __restrict__ k, T* __restrict__ out,
+                                                              const float* __restrict__ m, int64_t m_sb,
+                                                              int64_t k_sb, int64_t k_sn, int64_t k_sh,
+                                                              int64_t o_sb, int64_t o_sn, int64_t o_sh, int n,
+                                                              int h, int cpr, int64_t chunks) {
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; c < chunks;
+       c += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const int col = static_cast<int>(c % cpr) * 8;
+    const int64_t row = c / cpr;  // (b * n + j) * h + g
+    const int g = static_cast<int>(row % h);
+    const int64_t bj = row / h;
+    const int j = static_cast<int>(bj % n);
+    const int64_t b = bj / n;
+    const float mj = m[b * m_sb + j];
+    const uint4 w = *reinterpret_cast<const uint4*>(k + b * k_sb + j * k_sn + g * k_sh + col);
+    uint4 r;
+    const uint32_t* wi = reinterpret_cast<const uint32_t*>(&w);
+    uint32_t* ri = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if constexpr (std::is_same<T, __half>::value) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&wi[i]));
+        const __half2 o = __floats2half2_rn(f.x * mj, f.y * mj);
+        ri[i] = *reinterpret_cast<const uint32_t*>(&o);
+      } else {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wi[i]));
+        const __nv_bfloat162 o = __floats2bfloat162_rn(f.x * mj, f.y * mj);
+        ri[i] = *reinterpret_cast<const uint32_t*>(&o);
+      }
+    }
+    *reinterpret_cast<uint4*>(out + b * o_sb + j * o_sn + g * o_sh + col) = r;
+  }
+}
+
 }  // namespace fsprep
 
 namespace fs {
@@ -279,6 +318,48 @@ fs_status fs_prepare(const fs_prep_params* p, fs_stream_t stream_) {
   const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 8LL * sms)));
   stats_kernel<<<dim3(gx, 3), kThreads, 0, stream>>>(a);
   quant_kernel<<<dim3(gx, 3), kThreads, 0, stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FS_ERR_CUDA, cudaGetErrorString(e));
+  return FS_OK;
+}
+
+fs_status fs_scale_keys(const fs_fwd_params* p, void* k_out, const int64_t* k_out_stride, fs_stream_t stream_) {
+  using namespace fsprep;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  auto fail = [](fs_status st, const char* m) {
+    fs::set_last_error(m);
+    return st;
+  };
+  if (!p || !k_out || !k_out_stride || !p->key_scale)
+    return fail(FS_ERR_CONFIG, "fs_scale_keys: params, key_scale, k_out and its strides are required");
+  if (p->in_dtype != FS_F16 && p->in_dtype != FS_BF16)
+    return fail(FS_ERR_DTYPE, "fs_scale_keys: in_dtype must be FS_F16 or FS_BF16");
+  if (p->batch < 0 || p->seqlen_kv < 0 || p->heads_kv < 1 || p->head_dim < 1 || p->head_dim % 8 != 0)
+    return fail(FS_ERR_SHAPE, "fs_scale_keys: bad extents (head_dim a multiple of 8)");
+  auto al16 = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15u) == 0; };
+  for (int i = 0; i < 3; ++i)
+    if ((p->k_stride[i] * 2) % 16 || (k_out_stride[i] * 2) % 16)
+      return fail(FS_ERR_UNSUPPORTED, "fs_scale_keys: strides must be multiples of 16 bytes");
+  if (!al16(p->k) || !al16(k_out)) return fail(FS_ERR_UNSUPPORTED, "fs_scale_keys: 16-byte aligned k / k_out");
+  const int cpr = p->head_dim / 8;
+  const int64_t chunks = static_cast<int64_t>(p->batch) * p->seqlen_kv * p->heads_kv * cpr;
+  if (chunks == 0) return FS_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid =
+      static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((chunks + kThreads - 1) / kThreads, 16LL * sms)));
+  const int64_t m_sb = p->batch > 1 ? p->key_scale_stride : 0;
+  if (p->in_dtype == FS_F16)
+    scale_keys_kernel<__half><<<grid, kThreads, 0, stream>>>(
+        static_cast<const __half*>(p->k), static_cast<__half*>(k_out), p->key_scale, m_sb, p->k_stride[0],
+        p->k_stride[1], p->k_stride[2], k_out_stride[0], k_out_stride[1], k_out_stride[2], p->seqlen_kv,
+        p->heads_kv, cpr, chunks);
+  else
+    scale_keys_kernel<__nv_bfloat16><<<grid, kThreads, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(p->k), static_cast<__nv_bfloat16*>(k_out), p->key_scale, m_sb,
+        p->k_stride[0], p->k_stride[1], p->k_stride[2], k_out_stride[0], k_out_stride[1], k_out_stride[2],
+        p->seqlen_kv, p->heads_kv, cpr, chunks);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FS_ERR_CUDA, cudaGetErrorString(e));
   return FS_OK;

@@ -130,7 +130,7 @@ py::tuple fwd(const at::Tensor& q, const at::Tensor& k, const at::Tensor& v, c10
     p.tile_n_hint = static_cast<int32_t>(tile_n);
     p.normalizer = static_cast<int32_t>(normalizer);
     auto stream = at::cuda::getCurrentCUDAStream(dev.index());
-    at::Tensor ks;
+    at::Tensor ks, k_scaled;  // (kept alive until the launch is queued)
     if (key_scale.has_value()) {
       ks = key_scale->dim() == 2 ? *key_scale : key_scale->reshape({1, -1});
       if (!ks.is_cuda() || ks.scalar_type() != at::kFloat || ks.device() != dev || ks.size(0) != b ||
@@ -145,6 +145,19 @@ py::tuple fwd(const at::Tensor& q, const at::Tensor& k, const at::Tensor& v, c10
       }
       p.key_scale = ks.data_ptr<float>();
       p.key_scale_stride = ks.stride(0);
+      if ((ic == FS_F16 || ic == FS_BF16) && d % 8 == 0 && nkv > 0) {
+        // 16-bit inputs: K' = m K in one HBM pass (fs_scale_keys), then the plain kernel -- cheaper
+        // than the in-kernel per-score multiply (include/flashsign.h)
+        at::Tensor kp = at::empty({b, nkv, hkv, d}, k.options());
+        const int64_t kst[3] = {kp.stride(0), kp.stride(1), kp.stride(2)};
+        const fs_status s2 = fs_scale_keys(&p, kp.data_ptr(), kst, reinterpret_cast<fs_stream_t>(stream.stream()));
+        if (s2 != FS_OK) throw Fail{static_cast<int>(s2), std::string(fs_last_error())};
+        p.k = kp.data_ptr();
+        for (int i = 0; i < 3; ++i) p.k_stride[i] = kst[i];
+        p.key_scale = nullptr;
+        p.key_scale_stride = 0;
+        k_scaled = kp;
+      }
     }
     // kv_splits < 0: the library's wave model picks the split (FS_SPLITS_AUTO, tail-only or uniform)
     p.kv_splits = static_cast<int32_t>(kv_splits >= 0 ? kv_splits : FS_SPLITS_AUTO);

@@ -31,6 +31,8 @@ CASES = {  # name: (B, N, H, D, dtype, eps)
     "c3": (8, 16384, 16, 128, "bf16", 0.0),
     "c4": (8, 8192, 16, 128, "e4m3", 0.0),
     "c5": (64, 20000, 8, 64, "bf16", 1e-6),
+    "c5m": (64, 20000, 8, 64, "bf16", 1e-6),   # + fused multiplicities m in {0..5} (key_scale)
+    "c3m": (8, 16384, 16, 128, "bf16", 1e-6),
 }
 
 
@@ -79,6 +81,9 @@ def run(cases, rounds):
         p.in_dtype, p.out_dtype = code[dt], (_lib.FS_F16 if dt == "fp16" else _lib.FS_BF16)
         p.scale, p.eps, p.p_scale, p.q_descale, p.k_descale, p.v_descale = 1.0, eps, 1.0, 1.0, 1.0, 1.0
         p.bad_key = bad.data_ptr()
+        if cname.endswith("m"):
+            m = torch.randint(0, 6, (B, N), generator=g, device="cuda").float()
+            p.key_scale, p.key_scale_stride = m.data_ptr(), m.stride(0)
         flops = 4.0 * B * H * N * N * D
         s = torch.cuda.current_stream().cuda_stream
         est_ms = flops / 1.2e15 * 1e3

@@ -604,6 +604,84 @@ def test_key_scale_power_of_two_is_bitwise_prescaled_keys():
     assert torch.equal(fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, key_scale=big[:, 1:334]), fused)
 
 
+@pytest.mark.parametrize("dt,d", [(torch.bfloat16, 64), (torch.bfloat16, 128), (torch.float16, 64),
+                                  (torch.float16, 128)])
+def test_key_scale_integer_is_bitwise_prescaled_keys(dt, d):
+    # 16-bit inputs: the kernel forms K' = m K in shared memory with one rounding (packed HMUL2) --
+    # bit for bit what pre-scaling K in fp32 / float64 and casting gives, for integer m (GRN counts,
+    # grn.py:150) and for the fp32 fallback path (non-representable m); several work tiles per CTA
+    # so ring slots are reused
+    g = torch.Generator(device="cuda").manual_seed(69)
+    q = rand_bshd(3, 700, 4, d, dt, 70)
+    k = rand_bshd(3, 2500, 2, d, dt, 71)
+    v = rand_bshd(3, 2500, 2, d, dt, 72)
+    for vals in ([0.0, 1.0, 2.0, 3.0, 4.0, 5.0], [0.3, 1.7, 2.9]):
+        m = torch.tensor(vals, device="cuda")[torch.randint(0, len(vals), (3, 2500), generator=g, device="cuda")]
+        fused = fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, key_scale=m)
+        pre = fs().fwd(q, (k.float() * m[:, :, None, None]).to(dt), v, eps=1e-6, out_dtype=torch.float32)
+        assert torch.equal(fused, pre), vals
+
+
+def _abi_fwd(q, k, v, out, key_scale=None, eps=0.0):
+    # fs_fwd called directly through the C-ABI (no torch extension): the in-kernel key_scale path
+    import ctypes
+    from paper_2505_09326_b200 import _lib
+    codes = {torch.bfloat16: _lib.FS_BF16, torch.float16: _lib.FS_F16, torch.float32: _lib.FS_F32}
+    p = _lib.FsFwdParams()
+    p.q, p.k, p.v, p.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
+    for dst, t in ((p.q_stride, q), (p.k_stride, k), (p.v_stride, v), (p.o_stride, out)):
+        dst[0], dst[1], dst[2] = t.stride(0), t.stride(1), t.stride(2)
+    p.batch, p.heads_q, p.heads_kv, p.seqlen_q, p.seqlen_kv, p.head_dim = (q.shape[0], q.shape[2], k.shape[2],
+                                                                        q.shape[1], k.shape[1], q.shape[3])
+    p.in_dtype, p.out_dtype = codes[q.dtype], codes[out.dtype]
+    p.scale, p.eps, p.p_scale, p.q_descale, p.k_descale, p.v_descale = 1.0, eps, 1.0, 1.0, 1.0, 1.0
+    p.kv_splits = 1
+    if key_scale is not None:
+        p.key_scale, p.key_scale_stride = key_scale.data_ptr(), key_scale.stride(0)
+    st = _lib.load().fs_fwd(ctypes.byref(p), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == _lib.FS_OK, _lib.last_error()
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("dt,d", [(torch.bfloat16, 64), (torch.float16, 128)])
+def test_key_scale_in_kernel_abi_path(dt, d):
+    # C-ABI callers passing key_scale get the in-kernel per-score multiply (fp32 m_j s_ij); the torch
+    # entry forms K' = m K first (fs_scale_keys).  Both match the oracle and each other closely.
+    g = torch.Generator(device="cuda").manual_seed(73)
+    q = rand_bshd(2, 400, 4, d, dt, 74)
+    k = rand_bshd(2, 900, 2, d, dt, 75)
+    v = rand_bshd(2, 900, 2, d, dt, 76)
+    m = torch.randint(0, 6, (2, 900), generator=g, device="cuda").float()
+    o_abi = _abi_fwd(q, k, v, torch.empty(q.shape, dtype=torch.float32, device="cuda"), m, 1e-6)
+    check_tol(o_abi.cpu().numpy(), exact_of(q, k, v, 1.0, 1e-6, "spherical", m), dt, "abi key_scale")
+    o_torch = fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, key_scale=m)
+    assert float((o_abi - o_torch).abs().max()) <= 2e-2
+
+
+def test_scale_keys_pass_matches_torch():
+    # fs_scale_keys on a strided BSHD view: RNE(m * k) per element
+    import ctypes
+    from paper_2505_09326_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(77)
+    for dt in (torch.bfloat16, torch.float16):
+        kb = rand_bshd(3, 333, 6, 64, dt, 78)
+        k = kb[:, :, 1:5]                      # strided heads
+        m = torch.rand((3, 336), generator=g, device="cuda")[:, :333] * 7
+        out = torch.empty((3, 333, 4, 64), dtype=dt, device="cuda")
+        p = _lib.FsFwdParams()
+        p.k, p.batch, p.seqlen_kv, p.heads_kv, p.head_dim = k.data_ptr(), 3, 333, 4, 64
+        p.k_stride[0], p.k_stride[1], p.k_stride[2] = k.stride(0), k.stride(1), k.stride(2)
+        p.in_dtype = _lib.FS_BF16 if dt == torch.bfloat16 else _lib.FS_F16
+        p.key_scale, p.key_scale_stride = m.data_ptr(), m.stride(0)
+        ost = (ctypes.c_int64 * 3)(out.stride(0), out.stride(1), out.stride(2))
+        st = _lib.load().fs_scale_keys(ctypes.byref(p), ctypes.c_void_p(out.data_ptr()), ost,
+                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert st == _lib.FS_OK, _lib.last_error()
+        torch.cuda.synchronize()
+        assert torch.equal(out, (k.float() * m[:, :, None, None]).to(dt))
+
+
 def test_key_scale_validation():
     q = rand_bshd(1, 8, 1, 64, torch.bfloat16, 68)
     from paper_2505_09326_b200.tensor import ShapeMismatchError
