@@ -228,6 +228,19 @@ fs_status fs_prepare(const fs_prep_params *p, fs_stream_t stream);
    SM's shared-memory bandwidth, FS_KS_SMEM).  Async on `stream`. */
 fs_status fs_scale_keys(const fs_fwd_params *p, void *k_out, const int64_t *k_out_stride, fs_stream_t stream);
 
+/* The Gram (moment) form of the spherical contract (the identity behind
+   attention.py:146-200 for a2(u) = u^2): with G = sum_j k_j k_j^T and W = sum_j k_j v_j^T per (b, h_kv),
+       O_i = c q_i^T W / sqrt(c^2 q_i^T G q_i + eps)
+   -- the same function at 8 N d^2 instead of 4 N^2 d flops, HBM-bound.  Three tensor-core launches
+   (moments per key chunk; reduce into 16-bit hi + lo B-operand images; apply per 128-row query tile).
+   Same fs_fwd_params as fs_fwd (q, k, v, o, strides, extents, scale, eps, bad_key with fs_fwd's
+   first-bad-row key); FS_F16 / FS_BF16 inputs, head_dim a multiple of 8 (<= 128), the spherical
+   normaliser only, no key_scale (form K' first with fs_scale_keys), no splits / partials /
+   dev_scales.  `workspace`: device memory of fs_gram_workspace_bytes(p) bytes, 256-byte aligned.
+   Async on `stream`. */
+int64_t fs_gram_workspace_bytes(const fs_fwd_params *p);
+fs_status fs_gram_fwd(const fs_fwd_params *p, void *workspace, int64_t workspace_bytes, fs_stream_t stream);
+
 /* Thread-local text of the last non-FS_OK status. */
 const char *fs_last_error(void);
 

@@ -23,7 +23,8 @@ FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
 # every symbol include/flashsign.h declares
 EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version", "fs_kv_splits", "fs_partial_floats",
                     "fs_combine", "fs_peer_floats", "fs_fwd_peer", "fs_combine_peer", "fs_ipc_malloc", "fs_ipc_open",
-                    "fs_ipc_close", "fs_ipc_free", "fs_prepare", "fs_plan", "fs_scale_keys")
+                    "fs_ipc_close", "fs_ipc_free", "fs_prepare", "fs_plan", "fs_scale_keys",
+                    "fs_gram_workspace_bytes", "fs_gram_fwd")
 FS_SPLITS_AUTO = -1
 
 
@@ -184,6 +185,10 @@ def load() -> ctypes.CDLL:
             lib.fs_scale_keys.argtypes = [ctypes.POINTER(FsFwdParams), ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
                                           ctypes.c_void_p]
             lib.fs_scale_keys.restype = ctypes.c_int
+            lib.fs_gram_workspace_bytes.argtypes = [ctypes.POINTER(FsFwdParams)]
+            lib.fs_gram_workspace_bytes.restype = ctypes.c_int64
+            lib.fs_gram_fwd.argtypes = [ctypes.POINTER(FsFwdParams), ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+            lib.fs_gram_fwd.restype = ctypes.c_int
             _lib = lib
     return _lib
 

@@ -126,6 +126,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_KS_SMEM
 #define FS_KS_SMEM 0  // experiment: 16-bit multiplicities scaled in the K slot in shared memory (Cfg::KSM)
 #endif
+#ifndef FS_EXP_NOZ
+#define FS_EXP_NOZ 0  // experiment (wrong results): skip the norm warps' a2(s) accumulation
+#endif
 #ifndef FS_DEFER_Z
 #define FS_DEFER_Z 1  // 16-bit inputs: the norm warps' last-chunk a2(s) accumulation after the P hand-off
 #endif
@@ -800,7 +803,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // 8 chunks per thread in flight: loads first, then the multiplies, then the stores (one
         // chunk at a time would serialise on the shared-memory latency)
         constexpr int CPT = C::SLOT_BYTES / 16 / 64, NBT = 8;
-        static_assert(CPT % NBT == 0, "K slot chunks per scaler thread");
+        static_assert(!C::KSM || CPT % NBT == 0, "K slot chunks per scaler thread");
 #pragma unroll 1
         for (int b0 = 0; b0 < CPT; b0 += NBT) {
           uint4 w[NBT];
@@ -911,6 +914,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // sum of a2(s) over this half: packed FP32 FMAs / adds, two independent chains
         float2 h0 = make_float2(0.f, 0.f), h1 = h0;
         auto accum_a2 = [&](float2 a, float2 b) {
+          if constexpr (FS_EXP_NOZ) return;  // experiment (wrong z): what the a2(s) sums cost
           if constexpr (NORM == FS_NORM_SIGNED_L1) {
             h0 = __fadd2_rn(h0, make_float2(fabsf(a.x), fabsf(a.y)));
             h1 = __fadd2_rn(h1, make_float2(fabsf(b.x), fabsf(b.y)));
@@ -1013,7 +1017,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       // hand this half's z to the epilogue warpgroup and move on to the next work tile
-      const float z = (za.x + za.y) + (zb.x + zb.y);
+      const float z = (za.x + za.y) + (zb.x + zb.y) + (FS_EXP_NOZ ? 1.f : 0.f);
       ptx::mbar_wait(&bars->z_empty[t][ob], (static_cast<uint32_t>(it / C::NOB) & 1u) ^ 1u);
       zbuf[((t * C::NOB + ob) * 2 + hh0) * BM + r] = ovf ? __int_as_float(0x7f800000) : z;
       if (NWT == 4) zbuf[((t * C::NOB + ob) * 2 + 1) * BM + r] = 0.f;
@@ -1290,6 +1294,16 @@ static bool encode_bshd_uncached(CUtensorMap* map, CUtensorMapDataType dt, int e
     return false;
   }
   return true;
+}
+
+// for flashsign_gram.cu: the same (cached) BSHD tensor-map encoding
+bool encode_bshd_shared(CUtensorMap* map, int in_dtype, const void* ptr, int head_dim, int seqlen, int heads,
+                        int batch, const int64_t* stride, int box_w, int box_rows, std::string* err) {
+  const CUtensorMapDataType dt = in_dtype == FS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                 : in_dtype == FS_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                      : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  return encode_bshd(map, dt, in_dtype == FS_E4M3 ? 1 : 2, ptr, head_dim, seqlen, heads, batch, stride, box_w,
+                     box_rows, err);
 }
 
 static int kernel_d(const fs_fwd_params* p) { return (p->in_dtype == FS_E4M3 || p->head_dim > 64) ? 128 : 64; }

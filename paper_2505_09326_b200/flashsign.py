@@ -330,3 +330,80 @@ def kernel_score_tile(head_dim: int, dtype: torch.dtype = torch.bfloat16) -> int
     """Scores the kernel holds on chip per Q tile (128 rows x 128 / 192 keys, in TMEM)."""
     bm, bn = _lib.query_tile(min(max(head_dim, 1), 128), _IN_CODES[dtype])
     return bm * bn
+
+
+def _params_of(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor, scale: float, eps: float):
+    p = _lib.FsFwdParams()
+    p.q, p.k, p.v, p.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
+    for dst, t in ((p.q_stride, q), (p.k_stride, k), (p.v_stride, v), (p.o_stride, out)):
+        dst[0], dst[1], dst[2] = t.stride(0), t.stride(1), t.stride(2)
+    p.batch, p.heads_q, p.heads_kv = q.shape[0], q.shape[2], k.shape[2]
+    p.seqlen_q, p.seqlen_kv, p.head_dim = q.shape[1], k.shape[1], q.shape[3]
+    p.in_dtype, p.out_dtype = _IN_CODES[q.dtype], _OUT_CODES[out.dtype]
+    p.scale, p.eps, p.p_scale, p.q_descale, p.k_descale, p.v_descale = float(scale), float(eps), 1.0, 1.0, 1.0, 1.0
+    return p
+
+
+def scale_keys(k: torch.Tensor, key_scale: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """K' = m K (attention.py:381-388, grn.py:150) for 16-bit BSHD keys in one HBM pass (C-ABI
+    ``fs_scale_keys``): ``key_scale`` float32 ``[B, Nkv]``; fp32 product, then round to nearest even."""
+    if k.dtype not in (torch.bfloat16, torch.float16) or not k.is_cuda or k.dim() != 4 or k.stride(-1) != 1:
+        raise ShapeMismatchError("scale_keys: 16-bit BSHD CUDA keys with a contiguous head dim expected")
+    ks = key_scale.reshape(k.shape[0], -1) if key_scale.dim() == 1 else key_scale
+    if (ks.dtype != torch.float32 or tuple(ks.shape) != (k.shape[0], k.shape[1]) or ks.device != k.device
+            or (k.shape[1] > 0 and ks.stride(1) != 1)):
+        raise ShapeMismatchError("scale_keys: key_scale must be float32 [B, Nkv] on k's device")
+    if out is None:
+        out = torch.empty(k.shape, dtype=k.dtype, device=k.device)
+    p = _params_of(k, k, k, k, 1.0, 0.0)
+    p.key_scale, p.key_scale_stride = ks.data_ptr(), ks.stride(0)
+    ost = (ctypes.c_int64 * 3)(out.stride(0), out.stride(1), out.stride(2))
+    with torch.cuda.device(k.device):
+        st = _lib.load().fs_scale_keys(ctypes.byref(p), ctypes.c_void_p(out.data_ptr()), ost,
+                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if st != _lib.FS_OK:
+        raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
+    return out
+
+
+def gram_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, scale: float = 1.0, eps: float = 0.0,
+             out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
+             key_scale: torch.Tensor | None = None, check: bool = True,
+             bad_key: torch.Tensor | None = None) -> torch.Tensor:
+    """Spherical attention through its Gram (moment) form, C-ABI ``fs_gram_fwd`` (SURVEY.md section 0
+    fact 4): ``O_i = c q_i^T W / sqrt(c^2 q_i^T G q_i + eps)`` with ``G = K^T K``, ``W = K^T V`` per
+    (b, h_kv) -- the FlashSign contract (normalizers.py:94-100) at O(N d^2), three tensor-core
+    launches, HBM-bound.  16-bit BSHD inputs, spherical normaliser; ``key_scale`` multiplicities are
+    applied as K' = m K first (``scale_keys``).  ``check`` raises DegenerateDenominatorError for the
+    first bad row like ``fwd``."""
+    _check_inputs(q, k, v)
+    if q.dtype not in (torch.bfloat16, torch.float16):
+        raise ShapeMismatchError(f"gram_fwd: 16-bit inputs only, got {q.dtype}")
+    if q.shape[2] % k.shape[2]:
+        raise ConfigError(f"query heads must be a multiple of kv heads, got h={q.shape[2]}, h_kv={k.shape[2]}")
+    if key_scale is not None:
+        if check:
+            check_key_scale(key_scale)
+        k = scale_keys(k, key_scale)
+    if out_dtype is None:
+        out_dtype = out.dtype if out is not None else q.dtype
+    if out is None:
+        out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
+    elif tuple(out.shape) != tuple(q.shape) or out.dtype != out_dtype or out.stride(-1) != 1:
+        raise ShapeMismatchError(f"gram_fwd: bad out tensor {tuple(out.shape)} {out.dtype}")
+    if bad_key is None:
+        bad_key = torch.empty(1, dtype=torch.int64, device=q.device)
+    p = _params_of(q, k, v, out, scale, eps)
+    p.bad_key = bad_key.data_ptr()
+    lib = _lib.load()
+    with torch.cuda.device(q.device):
+        nbytes = int(lib.fs_gram_workspace_bytes(ctypes.byref(p)))
+        ws = torch.empty(max(nbytes, 256) + 256, dtype=torch.uint8, device=q.device)
+        base = (ws.data_ptr() + 255) & ~255
+        st = lib.fs_gram_fwd(ctypes.byref(p), ctypes.c_void_p(base), ctypes.c_int64(nbytes),
+                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if st != _lib.FS_OK:
+        raise _STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
+    if check:
+        raise_if_bad(bad_key, q.shape[2], q.shape[1])
+    return out

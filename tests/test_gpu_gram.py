@@ -1,0 +1,145 @@
+"""GPU parity of the Gram-form kernels (C-ABI ``fs_gram_fwd``; SURVEY.md section 0 fact 4 and
+section 8f #4) against the float64 oracle on the same 16-bit inputs.
+
+    O_i = c q_i^T W / sqrt(c^2 q_i^T G q_i + eps),  G = K^T K,  W = K^T V
+
+Float32 output: the moments are accumulated in fp32 on the tensor cores from exact 16-bit products
+and applied as hi + lo 16-bit terms (~2^-16 relative), so the result is far closer to the oracle
+than FlashSign's (whose P is rounded to the input dtype): rel-Frobenius <= 2e-4 in the test.
+16-bit output adds one rounding: the dtype's FlashSign tolerance applies.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.spherical import gram_batched
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2505_09326_b200 import build
+    build.build()
+
+
+def fs():
+    from paper_2505_09326_b200 import flashsign
+    return flashsign
+
+
+def rand_bshd(b, n, h, d, dtype, seed, scale=1.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn((b, n, h, d), generator=g, device="cuda") * scale).to(dtype)
+
+
+def oracle_of(q, k, v, scale=1.0, eps=0.0):
+    return gram_batched(q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy(), scale, eps)
+
+
+def rel_fro(got, ref):
+    got = np.asarray(got, np.float64)
+    return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+SHAPES = [  # (B, Nq, Nkv, H, Hkv, d)
+    (1, 128, 128, 1, 1, 128),
+    (1, 128, 128, 1, 1, 64),
+    (2, 300, 517, 4, 2, 128),    # ragged, GQA
+    (3, 777, 1000, 2, 1, 64),
+    (1, 200, 300, 2, 2, 96),     # head dim zero-filled to 128 by TMA
+    (1, 64, 64, 1, 1, 32),
+    (2, 1, 5, 3, 3, 64),         # one query row, a few keys
+    (1, 2048, 16384, 2, 1, 128),  # many key chunks per (b, h_kv)
+]
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16], ids=["bf16", "fp16"])
+@pytest.mark.parametrize("shape", SHAPES, ids=[str(s) for s in SHAPES])
+def test_gram_matches_oracle(shape, dt):
+    b, nq, nkv, h, hkv, d = shape
+    q = rand_bshd(b, nq, h, d, dt, 1)
+    k = rand_bshd(b, nkv, hkv, d, dt, 2)
+    v = rand_bshd(b, nkv, hkv, d, dt, 3)
+    ref = oracle_of(q, k, v, 1.0, 1e-6)
+    o = fs().gram_fwd(q, k, v, eps=1e-6, out_dtype=torch.float32)
+    assert rel_fro(o.cpu().numpy(), ref) <= 2e-4
+    o16 = fs().gram_fwd(q, k, v, eps=1e-6)
+    err = np.abs(o16.float().cpu().numpy() - ref)
+    assert err.max() <= (8e-3 if dt == torch.float16 else 5e-2) and np.mean(err <= 0.01) >= 0.99
+
+
+@pytest.mark.parametrize("scale", [0.125, -1.5, 3.0])
+def test_gram_scale_and_eps(scale):
+    q = rand_bshd(2, 256, 2, 64, torch.bfloat16, 4, scale=3.0)
+    k = rand_bshd(2, 700, 2, 64, torch.bfloat16, 5)
+    v = rand_bshd(2, 700, 2, 64, torch.bfloat16, 6)
+    for eps in (0.0, 0.5, 100.0):
+        o = fs().gram_fwd(q, k, v, scale=scale, eps=eps, out_dtype=torch.float32)
+        assert rel_fro(o.cpu().numpy(), oracle_of(q, k, v, scale, eps)) <= 2e-4
+
+
+def test_gram_large_magnitudes_fp16():
+    # the moments exceed fp16 range (|G| ~ N * 256^2): the reduce step's power-of-two scales keep
+    # the hi / lo images finite
+    q = rand_bshd(1, 256, 2, 64, torch.float16, 7, scale=16.0)
+    k = rand_bshd(1, 4096, 2, 64, torch.float16, 8, scale=16.0)
+    v = rand_bshd(1, 4096, 2, 64, torch.float16, 9, scale=16.0)
+    o = fs().gram_fwd(q, k, v, out_dtype=torch.float32)
+    assert rel_fro(o.cpu().numpy(), oracle_of(q, k, v)) <= 2e-4
+
+
+def test_gram_agrees_with_flashsign_kernel():
+    q = rand_bshd(2, 1000, 4, 128, torch.bfloat16, 10)
+    k = rand_bshd(2, 3000, 4, 128, torch.bfloat16, 11)
+    v = rand_bshd(2, 3000, 4, 128, torch.bfloat16, 12)
+    a = fs().gram_fwd(q, k, v, eps=1e-6, out_dtype=torch.float32)
+    b = fs().fwd(q, k, v, eps=1e-6, out_dtype=torch.float32)
+    assert float((a - b).abs().max()) <= 5e-2
+    assert rel_fro(b.cpu().numpy(), a.cpu().numpy().astype(np.float64)) <= 5e-3
+
+
+def test_gram_degenerate_rows_and_empty_keys():
+    from paper_2505_09326_b200.normalizers import DegenerateDenominatorError
+    q = rand_bshd(2, 300, 2, 64, torch.bfloat16, 13)
+    k = rand_bshd(2, 400, 1, 64, torch.bfloat16, 14)
+    v = rand_bshd(2, 400, 1, 64, torch.bfloat16, 15)
+    q[1, 77, 0] = 0
+    q[1, 150, 1] = 0
+    bad = torch.empty(1, dtype=torch.int64, device="cuda")
+    fs().gram_fwd(q, k, v, check=False, bad_key=bad)
+    assert fs().decode_bad_key(int(bad.item()), 2, 300) == (1, 0, 77, 0.0)
+    with pytest.raises(DegenerateDenominatorError, match="row 77"):
+        fs().gram_fwd(q, k, v)
+    # eps > 0 rescues the zero rows: O = 0 there
+    o = fs().gram_fwd(q, k, v, eps=1e-3, out_dtype=torch.float32)
+    assert float(o[1, 77, 0].abs().max()) == 0.0
+    # no keys: every row has z = 0
+    k0 = torch.empty((2, 0, 1, 64), dtype=torch.bfloat16, device="cuda")
+    fs().gram_fwd(q, k0, k0, check=False, bad_key=bad)
+    assert fs().decode_bad_key(int(bad.item()), 2, 300) == (0, 0, 0, 0.0)
+
+
+def test_gram_multiplicities_match_prescaled():
+    g = torch.Generator(device="cuda").manual_seed(16)
+    q = rand_bshd(2, 300, 4, 64, torch.bfloat16, 17)
+    k = rand_bshd(2, 900, 2, 64, torch.bfloat16, 18)
+    v = rand_bshd(2, 900, 2, 64, torch.bfloat16, 19)
+    m = torch.randint(0, 6, (2, 900), generator=g, device="cuda").float()
+    a = fs().gram_fwd(q, k, v, eps=1e-6, out_dtype=torch.float32, key_scale=m)
+    b = fs().gram_fwd(q, (k.float() * m[:, :, None, None]).to(k.dtype), v, eps=1e-6, out_dtype=torch.float32)
+    assert torch.equal(a, b)
+
+
+def test_gram_rejects_what_it_cannot_do():
+    from paper_2505_09326_b200._errors import ConfigError
+    from paper_2505_09326_b200.tensor import ShapeMismatchError
+    q = rand_bshd(1, 16, 1, 64, torch.bfloat16, 20)
+    with pytest.raises(ShapeMismatchError):
+        fs().gram_fwd(q.to(torch.float8_e4m3fn), q.to(torch.float8_e4m3fn), q.to(torch.float8_e4m3fn))
+    kv2 = rand_bshd(1, 16, 2, 64, torch.bfloat16, 22)
+    with pytest.raises(ConfigError):
+        fs().gram_fwd(rand_bshd(1, 16, 3, 64, torch.bfloat16, 21), kv2, kv2)
