@@ -364,7 +364,8 @@ def context_baselines(cfg, q, k, v, device, steps, device_index):
       * SDPA softmax attention, per backend (cuDNN, flash) -- the paper's "within 5 % of
         FlashAttention-2" claim (PAPER.md:201), on B200;
       * PyTorch-eager spherical attention (materialises S per (b, h); PAPER.md:199);
-      * the O(N d^2) Gram-form identity (a different algorithm, context only).
+      * the O(N d^2) Gram-form identity through our own kernels (fs_gram_fwd; a
+        different algorithm, reported beside, never under the 4 B H N^2 d metric).
     e4m3 configurations run the baselines in bf16 (no fp8 SDPA)."""
     import torch
     import torch.nn.functional as F
@@ -387,15 +388,12 @@ def context_baselines(cfg, q, k, v, device, steps, device_index):
                 z = s_.float().square().sum(-1, keepdim=True).sqrt()
                 (s_ @ v[b, :, hk]).float().div_(z)
 
-    def gram():
-        hk = torch.arange(H, device=q.device) * HKV // H
-        for b in range(B):
-            qh = q[b].float().transpose(0, 1)
-            kh = k[b].float().transpose(0, 1)[hk]
-            vh = v[b].float().transpose(0, 1)[hk]
-            kt_ = kh.transpose(1, 2)
-            z = (torch.bmm(qh, torch.bmm(kt_, kh)) * qh).sum(-1, keepdim=True).sqrt()
-            torch.bmm(qh, torch.bmm(kt_, vh)).div_(z)
+    from paper_2505_09326_b200 import flashsign
+    go = torch.empty(q.shape, dtype=q.dtype, device=q.device)
+    gbad = torch.empty(1, dtype=torch.int64, device=q.device)
+
+    def gram():  # our tensor-core Gram-form kernels (fs_gram_fwd), same inputs, same output dtype
+        flashsign.gram_fwd(q, k, v, eps=cfg["eps"], out=go, check=False, bad_key=gbad)
 
     fns = []
     try:
@@ -410,13 +408,17 @@ def context_baselines(cfg, q, k, v, device, steps, device_index):
                 ("sdpa_softmax_flash", pinned(SDPBackend.FLASH_ATTENTION), max(3, steps // 4))]
     except ImportError:
         fns.append(("sdpa_softmax", sdpa, steps))
-    fns += [("torch_eager_spherical", eager, 2), ("gram_form_fp32_not_flashsign", gram, 3)]
+    fns += [("torch_eager_spherical", eager, 2), ("gram_form_kernel_not_flashsign", gram, max(10, steps))]
     for name, fn, n in fns:
         try:
             ms, clk = _timed(fn, n, device_index)
             if name.startswith("gram"):
-                res[name] = {"ms_per_step": ms, "steps": n, "clocks": clk,
-                             "note": "O(N d^2) identity, not the 4*N^2*d FlashSign work"}
+                # HBM roofline of the Gram path: Q, K, V read and O written once
+                byts = sum(t.numel() * t.element_size() for t in (q, k, v, go))
+                res[name] = {"ms_per_step": ms, "steps": n, "clocks": clk, "hbm_gbs": byts / ms / 1e6,
+                             "bytes_per_step": byts, "speedup_vs_flashsign_step": None,
+                             "note": "fs_gram_fwd: the O(N d^2) moment form of the same spherical "
+                                     "contract (SURVEY.md 0 fact 4), not the 4*N^2*d FlashSign work"}
             else:
                 res[name] = {"tflops": fl / ms / 1e9, "ms_per_step": ms, "steps": n, "clocks": clk,
                              "dtype": str(q.dtype).replace("torch.", ""), "shape": "full configuration"}
@@ -717,6 +719,9 @@ def run_ours(args, cfg):
         ctx = None
         if world == 1 and not args.no_context:
             ctx = context_baselines(cfg, q, k, v, dev, args.steps, local)
+            gk = ctx.get("gram_form_kernel_not_flashsign", {})
+            if "ms_per_step" in gk:
+                gk["speedup_vs_flashsign_step"] = ms_step / gk["ms_per_step"]
         line = {
             "metric": "FlashSign fwd TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

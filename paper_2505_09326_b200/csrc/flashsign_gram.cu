@@ -12,7 +12,7 @@
 //   1. gram_kv_kernel     per (b, h_kv, key chunk): [G | W] partial = K^T [K | V] (d = 128) or
 //                         [K | V]^T K = [G ; W^T] (d = 64), kind::f16 with both operands MN-major
 //                         straight from the TMA tiles, fp32 in TMEM -> fp32 partials in global.
-//   2. gram_reduce_kernel per (b, h_kv): sum the chunks, split W^T and G into 16-bit hi + lo terms
+//   2. gram_reduce_kernel per (b, h_kv, 16 rows): sum the chunks, split W^T and G into 16-bit hi + lo terms
 //                         (x = hi + lo to ~2^-16 relative) under one power-of-two scale each, and
 //                         write them as the SW128 K-major shared-memory image of the B operand.
 //   3. gram_apply_kernel  persistent over (b, h, 128-row query tile): T = Q [W^T ; G]^T with both
@@ -61,6 +61,7 @@ struct KvCfg {
 
 struct KvArgs {
   float* partial;   // [items][128][N] fp32
+  float* amax;      // [B*H_kv][2] max |partial| of G, W over the chunks (zeroed before the launch)
   int n_chunks, chunk_tiles, n_kv_tiles, heads_kv;
 };
 
@@ -132,20 +133,36 @@ __global__ void __launch_bounds__(128, 1)
     ptx::tc_commit_p(done, lp);
   }
   __syncwarp();
-  float* dst = a.partial + static_cast<int64_t>(item) * 128 * C::N + (warp * 32 + lane) * C::N;
+  const int row = warp * 32 + lane;
+  float* dst = a.partial + static_cast<int64_t>(item) * 128 * C::N + row * C::N;
   if (t1 > t0) {
     ptx::mbar_wait(done, 0);
     ptx::tc_fence_after();
+    float mx[2] = {0.f, 0.f};  // G, W parts of this row
 #pragma unroll 1
     for (int c = 0; c < C::N / 32; ++c) {
       uint32_t r[32];
       ptx::tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 32, r);
       ptx::tmem_wait_ld();
+      float cm = 0.f;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        reinterpret_cast<float4*>(dst + c * 32)[k] =
-            make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]), __uint_as_float(r[4 * k + 2]),
-                        __uint_as_float(r[4 * k + 3]));
+      for (int k = 0; k < 8; ++k) {
+        const float4 f = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                                     __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+        reinterpret_cast<float4*>(dst + c * 32)[k] = f;
+        cm = fmaxf(cm, fmaxf(fmaxf(fabsf(f.x), fabsf(f.y)), fmaxf(fabsf(f.z), fabsf(f.w))));
+      }
+      if (D == 128 ? (c * 32 >= 128) : (row >= 64))
+        mx[1] = fmaxf(mx[1], cm);
+      else
+        mx[0] = fmaxf(mx[0], cm);
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx[m] = fmaxf(mx[m], __shfl_xor_sync(0xffffffffu, mx[m], o));
+      // non-negative floats order like their bit patterns
+      if (lane == 0) atomicMax(reinterpret_cast<int*>(a.amax) + 2 * bh + m, __float_as_int(mx[m]));
     }
   } else {
     for (int c = 0; c < C::N; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -185,58 +202,59 @@ __device__ __forceinline__ float from16(uint16_t x) {
   else return __half2float(__ushort_as_half(x));
 }
 
-// Launch 2: one CTA per (b, h_kv).  Sums the chunk partials in shared memory, picks one power-of-
-// two scale per moment (max |x 2^-e| < 2^14: fp16-safe), writes the hi / lo image and the scales.
+// Launch 2: grid (b*h_kv, 2d/16): each CTA writes 16 image rows.  A thread forms one 16-byte chunk
+// (8 elements) of a row: the chunk sums of the moments, one power-of-two scale per moment and
+// (b, h_kv) from launch 1's max |partial| (times the chunk count: a bound on max |sum|, keeping
+// |x 2^-e| < 2^14, fp16-safe), then hi = rn(x), lo = rn(x - hi).
+constexpr int RED_ROWS = 16;
+
 template <int IN, int D>
-__global__ void __launch_bounds__(256) gram_reduce_kernel(const float* __restrict__ partial, int n_chunks,
-                                                          uint16_t* __restrict__ img, float* __restrict__ scl) {
+__global__ void __launch_bounds__(128) gram_reduce_kernel(const float* __restrict__ partial, int n_chunks,
+                                                          const float* __restrict__ amax, uint16_t* __restrict__ img,
+                                                          float* __restrict__ scl) {
   constexpr int N = KvCfg<D>::N;
-  extern __shared__ float acc[];  // [128][N]
-  __shared__ float amax[2];
+  constexpr int CPR = D / 8;  // 16-byte chunks per image row
   const int bh = blockIdx.x;
-  if (threadIdx.x < 2) amax[threadIdx.x] = 0.f;
-  __syncthreads();
-  float mx[2] = {0.f, 0.f};
-  const float* src = partial + static_cast<int64_t>(bh) * n_chunks * 128 * N;
-  for (int e = threadIdx.x; e < 128 * N; e += blockDim.x) {
-    float s = 0.f;
-    for (int c = 0; c < n_chunks; ++c) s += src[static_cast<int64_t>(c) * 128 * N + e];
-    acc[e] = s;
-    const int r = e / N, col = e % N;
-    const bool is_w = D == 128 ? col >= 128 : r >= 64;  // which moment this element belongs to
-    mx[is_w] = fmaxf(mx[is_w], fabsf(s));
-  }
-  atomicMax(reinterpret_cast<int*>(&amax[0]), __float_as_int(mx[0]));  // non-negative floats order as ints
-  atomicMax(reinterpret_cast<int*>(&amax[1]), __float_as_int(mx[1]));
-  __syncthreads();
   int ex[2];
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
-    const float am = amax[m];
-    ex[m] = (am > 0.f && isfinite(am)) ? ilogbf(am) - 13 : 0;  // am * 2^-e in [2^13, 2^14)
+    const float am = amax[2 * bh + m] * static_cast<float>(n_chunks);
+    ex[m] = (am > 0.f && isfinite(am)) ? ilogbf(am) - 13 : 0;
   }
-  if (threadIdx.x == 0) {
+  if (blockIdx.y == 0 && threadIdx.x == 0) {
     scl[2 * bh + 0] = exp2f(static_cast<float>(ex[1]));  // W
     scl[2 * bh + 1] = exp2f(static_cast<float>(ex[0]));  // G
   }
+  const float* src = partial + static_cast<int64_t>(bh) * n_chunks * 128 * N;
   uint16_t* out = img + static_cast<int64_t>(bh) * (ImgCfg<D>::BYTES / 2);
-  for (int e = threadIdx.x; e < 2 * D * D; e += blockDim.x) {
-    const int n = e / D, k = e % D;  // image row n, column k
-    float x;
-    int m;  // 1 = W, 0 = G
-    if (n < D) {  // W^T[n][k] = W[k][n]
-      m = 1;
-      x = D == 128 ? acc[k * N + 128 + n] : acc[(64 + n) * N + k];
-    } else {
-      m = 0;
-      x = acc[(n - D) * N + k];
+  for (int e = threadIdx.x; e < RED_ROWS * CPR; e += blockDim.x) {
+    const int n = blockIdx.y * RED_ROWS + e / CPR, k0 = (e % CPR) * 8;
+    const int m = n < D ? 1 : 0;  // image rows: W^T first, then G
+    float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < n_chunks; ++c) {
+      const float* pc = src + static_cast<int64_t>(c) * 128 * N;
+      if (m == 0 || D == 64) {  // a contiguous run of one accumulator row
+        const float* r = m == 0 ? pc + (n - D) * N + k0 : pc + (64 + n) * N + k0;
+        const float4 u = *reinterpret_cast<const float4*>(r), w = *reinterpret_cast<const float4*>(r + 4);
+        x[0] += u.x; x[1] += u.y; x[2] += u.z; x[3] += u.w;
+        x[4] += w.x; x[5] += w.y; x[6] += w.z; x[7] += w.w;
+      } else {  // d = 128: W^T[n][k] = W[k][n], a column of the accumulator
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] += pc[(k0 + u) * N + 128 + n];
+      }
     }
-    x = ldexpf(x, -ex[m]);
-    const uint16_t hi = to16<IN>(x);
-    const uint16_t lo = to16<IN>(x - from16<IN>(hi));
-    const int off = img_offset<D>(n, k);
-    out[off] = hi;
-    out[ImgCfg<D>::TERM / 2 + off] = lo;
+    uint4 hi4, lo4;
+    uint16_t* hp = reinterpret_cast<uint16_t*>(&hi4);
+    uint16_t* lp = reinterpret_cast<uint16_t*>(&lo4);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float v = ldexpf(x[u], -ex[m]);
+      hp[u] = to16<IN>(v);
+      lp[u] = to16<IN>(v - from16<IN>(hp[u]));
+    }
+    const int off = img_offset<D>(n, k0);  // k0 % 8 == 0: the chunk's first element
+    *reinterpret_cast<uint4*>(out + off) = hi4;
+    *reinterpret_cast<uint4*>(out + ImgCfg<D>::TERM / 2 + off) = lo4;
   }
 }
 
@@ -481,7 +499,7 @@ static Plan plan_of(const fs_fwd_params* p) {
   pl.items = static_cast<int>(bhkv * pl.n_chunks);
   pl.partial_floats = static_cast<int64_t>(pl.items) * 128 * (pl.d == 128 ? 256 : 64);
   pl.img_bytes = bhkv * (pl.d == 128 ? ImgCfg<128>::BYTES : ImgCfg<64>::BYTES);
-  pl.scl_floats = 2 * bhkv;
+  pl.scl_floats = 4 * bhkv;  // scales, then the moments' max |partial|
   return pl;
 }
 
@@ -496,6 +514,11 @@ static fs_status run(const fs_fwd_params* p, const Plan& pl, uint8_t* ws, cudaSt
   float* partial = reinterpret_cast<float*>(ws);
   uint16_t* img = reinterpret_cast<uint16_t*>(ws + align256(pl.partial_floats * 4));
   float* scl = reinterpret_cast<float*>(ws + align256(pl.partial_floats * 4) + align256(pl.img_bytes));
+  float* amax = scl + pl.scl_floats / 2;
+  if (cudaMemsetAsync(amax, 0, sizeof(float) * pl.scl_floats / 2, stream) != cudaSuccess) {
+    *err = "cudaMemsetAsync failed";
+    return FS_ERR_CUDA;
+  }
   CUtensorMap tk, tv, tq;
   if (!encode_bshd_shared(&tk, IN, p->k, p->head_dim, p->seqlen_kv, p->heads_kv, p->batch, p->k_stride, 64, BK,
                           err) ||
@@ -507,15 +530,13 @@ static fs_status run(const fs_fwd_params* p, const Plan& pl, uint8_t* ws, cudaSt
   {
     auto kern = gram_kv_kernel<IN, D>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, KvCfg<D>::SMEM);
-    KvArgs a{partial, pl.n_chunks, pl.chunk_tiles, pl.n_kv_tiles, p->heads_kv};
+    KvArgs a{partial, amax, pl.n_chunks, pl.chunk_tiles, pl.n_kv_tiles, p->heads_kv};
     kern<<<pl.items, 128, KvCfg<D>::SMEM, stream>>>(tk, tv, a);
   }
   // 2. reduce + image
   {
-    auto kern = gram_reduce_kernel<IN, D>;
-    const int sm = 128 * KvCfg<D>::N * 4;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    kern<<<p->batch * p->heads_kv, 256, sm, stream>>>(partial, pl.n_chunks, img, scl);
+    gram_reduce_kernel<IN, D><<<dim3(p->batch * p->heads_kv, 2 * D / RED_ROWS), 128, 0, stream>>>(
+        partial, pl.n_chunks, amax, img, scl);
   }
   // 3. apply
   {
