@@ -325,8 +325,9 @@ def _run_reference(args, cfg):
         if i >= args.warmup:
             times.append((dt, fl))
     tot_t = sum(t for t, _ in times)
-    tot_f = sum(f for _, f in times)
-    val = tot_f / tot_t / 1e12
+    # median of the per-step rates: robust to host noise, and the statistic the ours-arm's
+    # cpu_baseline reports on the same sample size (so the two CPU numbers are comparable)
+    val = statistics.median(f / t for t, f in times) / 1e12
     sample = (f"{rows} query positions x {cfg['H']} heads x {cfg['N']} keys x d{cfg['D']} of one batch element "
               f"per step, float32 holding {cfg['dtype']} values, tile 64x64: {what}")
     line = {
@@ -706,15 +707,17 @@ def run_ours(args, cfg):
         if world == 1 and not args.no_cpu:
             rows = args.cpu_rows or reference_rows(cfg)
             with _all_host_threads():
-                tt_, ff_ = 0.0, 0.0
+                tt_, rates = 0.0, []
                 cpu_reference_sample(cfg, rows, seed=6)  # warm-up, like the reference arm's
-                for rep_ in range(3):  # same sample as one step of the reference arm, three times
+                for rep_ in range(5):  # same sample as one step of the reference arm, five times
                     dt, fl, threads, kind, what = cpu_reference_sample(cfg, rows, seed=7 + rep_)
-                    tt_, ff_ = tt_ + dt, ff_ + fl
+                    tt_ += dt
+                    rates.append(fl / dt)
                 host = _host_info()
-            cpu = {"value": ff_ / tt_ / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
-                   "sample": f"1 warm-up + 3 x ({rows} query positions x {H} heads x {N} keys x d{D} of one batch element), "
-                             f"float32 holding {cfg['dtype']} values, tile 64x64: {what}; {tt_:.2f} s",
+            cpu = {"value": statistics.median(rates) / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
+                   "sample": f"1 warm-up + 5 x ({rows} query positions x {H} heads x {N} keys x d{D} of one batch "
+                             f"element), median rate, float32 holding {cfg['dtype']} values, tile 64x64: {what}; "
+                             f"{tt_:.2f} s",
                    "cpu_count": os.cpu_count(), **host}
         ctx = None
         if world == 1 and not args.no_context:
