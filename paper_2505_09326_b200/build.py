@@ -81,7 +81,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(OUT_DIR, exist_ok=True)
     tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    # FLASHSIGN_NVCC_EXTRA: diagnostic builds only (e.g. a longer mbarrier watchdog under racecheck)
+    extra = os.environ.get("FLASHSIGN_NVCC_EXTRA", "").split()
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
