@@ -241,6 +241,28 @@ fs_status fs_scale_keys(const fs_fwd_params *p, void *k_out, const int64_t *k_ou
 int64_t fs_gram_workspace_bytes(const fs_fwd_params *p);
 fs_status fs_gram_fwd(const fs_fwd_params *p, void *workspace, int64_t workspace_bytes, fs_stream_t stream);
 
+/* Float64 streamed FlashSign for float32 / float64 callers of the drop-in API: the reference's
+   own loop (attention.py:146-200) with its rounding points -- float64 scores, or for a float32
+   grid (f32_grid = 1) scores rounded to float32 and scaled in float32 (attention.py:163-166) and
+   float32 squares summed in float64 (attention.py:188) -- on the SM's FP64 units, keys
+   accumulated in order for every row.  Reaches the reference's float64 tolerances (the tensor-core
+   fs_fwd cannot); a precision mode, not the hot path.  Layout as fs_fwd (BSHD, element strides,
+   head_dim <= 128); output float64; optional per-row z (float64, [B][H][Nq]) for the exception
+   text; bad_key as in fs_fwd.  Async on `stream`. */
+typedef struct {
+  const double *q, *k, *v;
+  double *o;
+  int64_t q_stride[3], k_stride[3], v_stride[3], o_stride[3];
+  int32_t batch, heads_q, heads_kv, seqlen_q, seqlen_kv, head_dim;
+  double scale, eps;   /* score scale c (finite), denom_epsilon >= 0 */
+  int32_t normalizer;  /* fs_normalizer */
+  int32_t f32_grid;    /* 1: the caller's arrays are float32 (the reference's float32 rounding points) */
+  uint64_t *bad_key;   /* optional device scalar, as fs_fwd */
+  double *z_out;       /* optional device [B*H*Nq]: each row's z */
+} fs_exact_params;
+
+fs_status fs_exact_fwd(const fs_exact_params *p, fs_stream_t stream);
+
 /* Thread-local text of the last non-FS_OK status. */
 const char *fs_last_error(void);
 

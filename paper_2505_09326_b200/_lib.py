@@ -24,7 +24,7 @@ FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
 EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version", "fs_kv_splits", "fs_partial_floats",
                     "fs_combine", "fs_peer_floats", "fs_fwd_peer", "fs_combine_peer", "fs_ipc_malloc", "fs_ipc_open",
                     "fs_ipc_close", "fs_ipc_free", "fs_prepare", "fs_plan", "fs_scale_keys",
-                    "fs_gram_workspace_bytes", "fs_gram_fwd")
+                    "fs_gram_workspace_bytes", "fs_gram_fwd", "fs_exact_fwd")
 FS_SPLITS_AUTO = -1
 
 
@@ -83,6 +83,33 @@ class FsPlanInfo(ctypes.Structure):
         ("partial_floats", ctypes.c_int64),
         ("busiest_steps", ctypes.c_double),
         ("efficiency", ctypes.c_double),
+    ]
+
+
+class FsExactParams(ctypes.Structure):
+    """Mirror of ``fs_exact_params`` (include/flashsign.h)."""
+
+    _fields_ = [
+        ("q", ctypes.c_void_p),
+        ("k", ctypes.c_void_p),
+        ("v", ctypes.c_void_p),
+        ("o", ctypes.c_void_p),
+        ("q_stride", ctypes.c_int64 * 3),
+        ("k_stride", ctypes.c_int64 * 3),
+        ("v_stride", ctypes.c_int64 * 3),
+        ("o_stride", ctypes.c_int64 * 3),
+        ("batch", ctypes.c_int32),
+        ("heads_q", ctypes.c_int32),
+        ("heads_kv", ctypes.c_int32),
+        ("seqlen_q", ctypes.c_int32),
+        ("seqlen_kv", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("scale", ctypes.c_double),
+        ("eps", ctypes.c_double),
+        ("normalizer", ctypes.c_int32),
+        ("f32_grid", ctypes.c_int32),
+        ("bad_key", ctypes.c_void_p),
+        ("z_out", ctypes.c_void_p),
     ]
 
 
@@ -189,6 +216,8 @@ def load() -> ctypes.CDLL:
             lib.fs_gram_workspace_bytes.restype = ctypes.c_int64
             lib.fs_gram_fwd.argtypes = [ctypes.POINTER(FsFwdParams), ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
             lib.fs_gram_fwd.restype = ctypes.c_int
+            lib.fs_exact_fwd.argtypes = [ctypes.POINTER(FsExactParams), ctypes.c_void_p]
+            lib.fs_exact_fwd.restype = ctypes.c_int
             _lib = lib
     return _lib
 

@@ -54,11 +54,15 @@ __all__ = [
 _COMPUTE_DTYPES = {"fp16": torch.float16, "bf16": torch.bfloat16}
 if hasattr(torch, "float8_e4m3fn"):
     _COMPUTE_DTYPES["e4m3"] = torch.float8_e4m3fn
+# "f64": the reference's own loop and rounding points on the FP64 units (C-ABI fs_exact_fwd) --
+# float64 tolerances for float32 / float64 callers, at FP64 speed instead of tensor-core speed
+_COMPUTE_DTYPES["f64"] = torch.float64
 _compute = os.environ.get("FLASHSIGN_COMPUTE_DTYPE", "fp16")
 
 
 def set_compute_dtype(name: str) -> None:
-    """Select the tensor-core input dtype for float32/float64 arrays: fp16 | bf16 | e4m3."""
+    """Select the compute mode for float32/float64 arrays: tensor-core operands fp16 | bf16 | e4m3, or
+    f64 (the reference's float64 loop on the FP64 units, fs_exact_fwd)."""
     global _compute
     if name not in _COMPUTE_DTYPES:
         raise ConfigError(f"compute dtype must be one of {sorted(_COMPUTE_DTYPES)}, got {name!r}")
@@ -181,6 +185,8 @@ def _gpu_streamed(q3: np.ndarray, k3: np.ndarray, v3: np.ndarray, scale: float, 
         return np.empty((0, h, d), dtype=out_np_dtype)
     if d > 128:
         raise ConfigError(f"flashsign: head dim {d} > 128 is not supported by the sm_100a kernel")
+    if compute == "f64" and not exact:
+        return _gpu_exact(q3, k3, v3, scale, eps, normalizer, m, out_np_dtype)
     dev = _device()
     src = [a if a.dtype in (np.float16, np.float32, np.float64) else a.astype(np.float64) for a in (q3, k3, v3)]
     if m is not None:
@@ -192,6 +198,44 @@ def _gpu_streamed(q3: np.ndarray, k3: np.ndarray, v3: np.ndarray, scale: float, 
         _, row, z = first
         raise DegenerateDenominatorError(float(z), f"row {row}")
     return out
+
+
+def _gpu_exact(q3: np.ndarray, k3: np.ndarray, v3: np.ndarray, scale: float, eps: float, normalizer: str,
+               m: np.ndarray | None, out_np_dtype) -> np.ndarray:
+    """The ``f64`` compute mode: the reference's streamed loop in float64 on the GPU (C-ABI
+    ``fs_exact_fwd``, csrc/flashsign_exact.cu) with the reference's float32 rounding points for
+    float32 arrays (attention.py:163-166, 188); first bad (head, row) as the reference reports it."""
+    import ctypes
+
+    from . import _lib
+    dev = _device()
+    n, h, d = q3.shape
+    x, h_kv, _ = k3.shape
+    kk = np.asarray(k3, dtype=np.float64)
+    if m is not None:
+        kk = kk * np.asarray(m, dtype=np.float64)[:, None, None]
+    q, k, v = (torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)[None] for a in (q3, kk, v3))
+    o = torch.empty(q.shape, dtype=torch.float64, device=dev)
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+    zrows = torch.empty(max(1, h * n), dtype=torch.float64, device=dev)
+    p = _lib.FsExactParams()
+    p.q, p.k, p.v, p.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr()
+    for dst, t in ((p.q_stride, q), (p.k_stride, k), (p.v_stride, v), (p.o_stride, o)):
+        dst[0], dst[1], dst[2] = t.stride(0), t.stride(1), t.stride(2)
+    p.batch, p.heads_q, p.heads_kv, p.seqlen_q, p.seqlen_kv, p.head_dim = 1, h, h_kv, n, x, d
+    p.scale, p.eps = float(scale), float(eps)
+    p.normalizer = flashsign.NORMALIZERS[normalizer]
+    p.f32_grid = 1 if q3.dtype == np.float32 else 0
+    p.bad_key, p.z_out = bad.data_ptr(), zrows.data_ptr()
+    with torch.cuda.device(dev):
+        st = _lib.load().fs_exact_fwd(ctypes.byref(p), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if st != _lib.FS_OK:
+        raise flashsign._STATUS_EXC.get(st, RuntimeError)(f"flashsign: {_lib.last_error()}")
+    info = flashsign.decode_bad_key(int(bad.item()), h, n)
+    if info is not None:
+        _, head, row, _ = info
+        raise DegenerateDenominatorError(float(zrows[head * n + row].item()), f"row {row}")
+    return o[0].cpu().numpy().astype(out_np_dtype, copy=False)
 
 
 def _record_tile(meter, tile, y: int, x: int, f16: bool) -> None:
@@ -276,8 +320,8 @@ def multiplicity_attention_array(q: np.ndarray, k: np.ndarray, v: np.ndarray, m,
     (grn.py:150 + 171-173; attention.py:381-388, 318-361) in one call.  Same validation and
     errors as the two reference calls (ShapeMismatchError for a length mismatch, ValueError
     for negative or non-finite m).  K' = m K is formed in float64 before the single rounding
-    to the compute dtype; the torch entry ``flashsign.fwd(key_scale=m)`` instead scales each
-    score inside the kernel (no K' at all, but slower on the d=64 GRN shape).
+    to the compute dtype (the torch entry ``flashsign.fwd(key_scale=m)`` forms it on the device in
+    one HBM pass, ``fs_scale_keys``).
     """
     mv = np.asarray(m, dtype=np.float64)
     if mv.ndim != 1 or k.ndim < 1 or mv.shape[0] != k.shape[0]:

@@ -54,7 +54,7 @@ def test_library_is_sm100a_with_tcgen05():
 
 @pytest.mark.parametrize("cname,cls", [("fs_fwd_params", _lib.FsFwdParams), ("fs_peer_params", _lib.FsPeerParams),
                                        ("fs_prep_tensor", _lib.FsPrepTensor), ("fs_prep_params", _lib.FsPrepParams),
-                                       ("fs_plan_info", _lib.FsPlanInfo)])
+                                       ("fs_plan_info", _lib.FsPlanInfo), ("fs_exact_params", _lib.FsExactParams)])
 def test_struct_layout_matches_header(tmp_path, cname, cls):
     fields = [f[0] for f in cls._fields_]
     prog = tmp_path / "layout.c"

@@ -64,7 +64,7 @@ def _env():
     return env
 
 
-def run_reference_tests(files, plugin=True, extra=()):
+def run_reference_tests(files, plugin=True, extra=(), env_extra=None):
     """Run reference test files; returns {nodeid: 'passed' | 'failed' | 'skipped'}."""
     xml = os.path.join(REF, f"junit_{os.getpid()}.xml")
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", f"--junitxml={xml}",
@@ -72,7 +72,9 @@ def run_reference_tests(files, plugin=True, extra=()):
     if plugin:
         cmd += ["-p", "ref_dropin_plugin"]
     cmd += [os.path.join(REF_TESTS, f) for f in files]
-    proc = subprocess.run(cmd, cwd=REF_TESTS, env=_env(), capture_output=True, text=True, timeout=3000)
+    env = _env()
+    env.update(env_extra or {})
+    proc = subprocess.run(cmd, cwd=REF_TESTS, env=env, capture_output=True, text=True, timeout=3000)
     out = {}
     try:
         for tc in ET.parse(xml).getroot().iter("testcase"):
@@ -142,3 +144,28 @@ def test_reference_suite_on_gpu():
                  "test_acceptance.py::test_criterion_4_f16_numerical_accuracy_analogue",
                  "test_acceptance.py::test_criterion_5_memory_claim"):
         assert res.get(must) == "passed", (must, res.get(must))
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_reference_suite_on_gpu_f64_mode():
+    """The same unmodified files with the drop-in API in its ``f64`` compute mode
+    (FLASHSIGN_COMPUTE_DTYPE=f64: the reference's loop and rounding points on the FP64 units,
+    fs_exact_fwd): the float64-tolerance assertions that the tensor-core mode cannot meet pass too.
+    Only the matplotlib-dependent tests (absent offline; they fail on the unpatched reference too)
+    may fail."""
+    files = ["test_attention.py", "test_grn.py", "test_acceptance.py"]
+    res = run_reference_tests(files, env_extra={"FLASHSIGN_COMPUTE_DTYPE": "f64"})
+    failed = sorted(k for k, v in res.items() if v == "failed")
+    summary = {
+        "mode": "f64 (fs_exact_fwd)",
+        "passed": sorted(k for k, v in res.items() if v == "passed"),
+        "failed": failed,
+        "counts": {s: sum(1 for v in res.values() if v == s) for s in ("passed", "failed", "skipped")},
+    }
+    out = os.environ.get("FS_REFSUITE_OUT_F64")
+    if out:
+        with open(out, "w") as f:
+            json.dump(summary, f, indent=1)
+    unexpected = [k for k in failed if not k.startswith(NO_MATPLOTLIB_PREFIX)]
+    assert not unexpected, unexpected
