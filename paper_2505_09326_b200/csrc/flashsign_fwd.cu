@@ -129,6 +129,13 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_EXP_NOZ
 #define FS_EXP_NOZ 0  // experiment (wrong results): skip the norm warps' a2(s) accumulation
 #endif
+#ifndef FS_ZP
+// 16-bit inputs: z = sum a2(p) over the packed P the PV MMA reads, accumulated after P is handed
+// over (mixed-precision FHFMA straight from the packed halves, re-read from TMEM), so the norm
+// step's critical path is only the conversion; the issuer waits for that re-read (s_free) before
+// the next QK overwrites the columns
+#define FS_ZP 0  // measured slower: experiment knob
+#endif
 #ifndef FS_DEFER_Z
 #define FS_DEFER_Z 1  // 16-bit inputs: the norm warps' last-chunk a2(s) accumulation after the P hand-off
 #endif
@@ -262,6 +269,7 @@ struct Cfg {
   // forms K' in one HBM pass (fs_scale_keys); FP8 keeps the per-score multiply (its norm step is
   // bound by the e4m3 conversion pipe, where the FMUL2s hide).
   static constexpr bool KSM = KS && !TR::F8 && FS_KS_SMEM;
+  static constexpr bool ZP = FS_ZP && !TR::F8;  // z from the packed P (see FS_ZP)
   static constexpr int KROWS = P2 ? BN / 2 : BN;                   // K rows in a CTA's slot
   static constexpr int VROW_BYTES = P2 ? ROW_BYTES / 2 : ROW_BYTES;  // bytes per key in a CTA's V slot
   static constexpr int V_SW = (VROW_BYTES % 128 == 0) ? 128 : 64;  // V slot swizzle span (B)
@@ -323,6 +331,7 @@ struct Bars {
   uint64_t ks_full[16];     // Cfg::KSM: the K slot holds m_j K_j (warps 2 and 3 arrived)
   uint64_t s_full[2];       // per S buffer (= Q tile)
   uint64_t p_full[2];       // per S buffer: all norm warps of the tile (both CTAs of a pair) wrote P
+  uint64_t s_free[2];       // per S buffer (FS_ZP): the norm warps re-read their P; the next QK may write
   uint64_t o_full[NQT][2], o_empty[NQT][2];
   uint64_t z_full[NQT][2], z_empty[NQT][2];
   uint32_t tmem_base;
@@ -351,6 +360,33 @@ __device__ __forceinline__ uint32_t pack4_e4m3(float a, float b, float c, float 
       : "=r"(r)
       : "f"(a), "f"(b), "f"(c), "f"(d));
   return r;
+}
+
+// z += lo^2 + hi^2 of a packed 16-bit pair, in fp32 (FHFMA: mixed-precision, no unpacking)
+template <int IN>
+__device__ __forceinline__ float fma_sq_hi_lo(uint32_t w, float z) {
+  if constexpr (IN == FS_BF16)
+    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\t"
+        "fma.rn.f32.bf16 %0, lo, lo, %0;\n\tfma.rn.f32.bf16 %0, hi, hi, %0;\n\t}"
+        : "+f"(z) : "r"(w));
+  else
+    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\t"
+        "fma.rn.f32.f16 %0, lo, lo, %0;\n\tfma.rn.f32.f16 %0, hi, hi, %0;\n\t}"
+        : "+f"(z) : "r"(w));
+  return z;
+}
+// z += |lo| + |hi| (the sign bits already cleared) as lo*1 + hi*1
+template <int IN>
+__device__ __forceinline__ float fma_abs_hi_lo(uint32_t w, float z) {
+  if constexpr (IN == FS_BF16)
+    asm("{\n\t.reg .b16 lo, hi, one;\n\tmov.b32 {lo, hi}, %1;\n\tmov.b16 one, 0x3F80;\n\t"
+        "fma.rn.f32.bf16 %0, lo, one, %0;\n\tfma.rn.f32.bf16 %0, hi, one, %0;\n\t}"
+        : "+f"(z) : "r"(w));
+  else
+    asm("{\n\t.reg .b16 lo, hi, one;\n\tmov.b32 {lo, hi}, %1;\n\tmov.b16 one, 0x3C00;\n\t"
+        "fma.rn.f32.f16 %0, lo, one, %0;\n\tfma.rn.f32.f16 %0, hi, one, %0;\n\t}"
+        : "+f"(z) : "r"(w));
+  return z;
 }
 
 template <int OUT>
@@ -456,6 +492,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&bars->s_full[b], 1);
       ptx::mbar_init(&bars->p_full[b], C::P2 ? 16 : 8);  // 2 column halves x 4 lane quarters (x 2 CTAs)
+      ptx::mbar_init(&bars->s_free[b], C::P2 ? 16 : 8);
     }
 #pragma unroll
     for (int t = 0; t < NQT; ++t) {
@@ -636,6 +673,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       {
       uint32_t kv_i = 0;                 // ring position of this work tile's K_0
       uint32_t p_use[NQT] = {0u, 0u};    // completed phases of p_full[t]
+      uint32_t qk_use[NQT] = {0u, 0u};   // QKs issued into S_t (ZP: each after the previous P's re-read)
       // the previous work tile's last PV_1, carried over the tile boundary (Cfg::CARRY)
       bool pend = false;
       uint32_t pend_slot = 0, pend_o_use = 0;
@@ -651,6 +689,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // S_t = Q_t K^T over the BN keys of the slot
         auto qk = [&](int t, uint32_t slot) {
           constexpr uint32_t idesc = C::IDESC_QK;
+          if constexpr (C::ZP) {
+            if (qk_use[t] > 0) {
+              if constexpr (C::P2)
+                ptx::mbar_wait_cluster(&bars->s_free[t], (qk_use[t] - 1) & 1u);
+              else
+                ptx::mbar_wait(&bars->s_free[t], (qk_use[t] - 1) & 1u);
+              ptx::tc_fence_after();
+            }
+            ++qk_use[t];
+          }
           const uint64_t a0 = q_desc + static_cast<uint32_t>(((t * C::NQB + qb) * C::Q_TILE_BYTES) >> 4);
           const uint64_t b0 = k_desc + static_cast<uint32_t>((slot * C::SLOT_BYTES) >> 4);
           const uint32_t d_tmem = tmem + C::COL_S0 + t * BN;
@@ -868,6 +916,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const float ps = p.dev_scales != nullptr ? p.dev_scales[3] : p.p_scale;
     // a half whose sum of a2(s) stays below this cannot hold an out-of-range P: (PMAX/|p_scale|)^{2|1}
     const float ovf_z = NORM == FS_NORM_SIGNED_L1 ? TR::PMAX / fabsf(ps) : (TR::PMAX / fabsf(ps)) * (TR::PMAX / fabsf(ps));
+    // ZP: z over P = p_scale * s is in P units; back to the operands' units (raw)
+    const float inv_pz = NORM == FS_NORM_SIGNED_L1 ? 1.f / ps : 1.f / (ps * ps);
     uint32_t s_use = 0;
 #if FS_PROF
     long long pr_sw = 0, pr_nc = 0, pr_nn = 0;
@@ -904,7 +954,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         constexpr int NCH = BN / 64;
         // 16-bit P, 192-key tiles: accumulate the last chunk's a2(s) after the P hand-off (FP8: the e4m3 conversion
         // runs on its own pipe and hides the FFMA2s; its saturation check needs the sums first)
-        constexpr bool DEFER_Z = FS_DEFER_Z && !TR::F8 && NCH >= 3;
+        constexpr bool DEFER_Z = FS_DEFER_Z && !TR::F8 && NCH >= 3 && !C::ZP;
         uint32_t s[32];
         ptx::tmem_ld32(s_addr, s);
         ptx::tmem_wait_ld();
@@ -942,7 +992,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               s[i + 2] = __float_as_uint(b.x);
               s[i + 3] = __float_as_uint(b.y);
             }
-            if (!(DEFER_Z && ch == NCH - 1)) accum_a2(a, b);
+            if (!C::ZP && !(DEFER_Z && ch == NCH - 1)) accum_a2(a, b);
           }
           // pack P (s[i] is written only after s[2i], s[2i+1] / s[4i..4i+3] are read)
           uint32_t pk_local[16];
@@ -974,7 +1024,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tmem_st16(s_addr + ch * 16, pk);
           if (ch + 1 < NCH) ptx::tmem_wait_ld();
         }
-        if constexpr (!DEFER_Z) {
+        if constexpr (!DEFER_Z && !C::ZP) {
           za = __fadd2_rn(za, h0);
           zb = __fadd2_rn(zb, h1);
         }
@@ -999,6 +1049,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_arrive_cluster(lead(&bars->p_full[sb]));  // the pair leader issues PV
           else
             ptx::mbar_arrive(&bars->p_full[sb]);
+        }
+        if constexpr (C::ZP) {
+          // z from the packed P this warp just handed to the MMA (the values the PV products use):
+          // re-read its BN/4 columns, release S_t for the next QK, then a2(p) in fp32 with
+          // mixed-precision FMAs straight from the 16-bit halves (two pairs of chains)
+          constexpr int PC = BN / 4;  // 32-bit P columns of this warp's half
+          uint32_t pw[PC];
+          ptx::tmem_ld32(s_addr, pw);
+          if constexpr (PC > 32) ptx::tmem_ld16(s_addr + 32, pw + 32);
+          ptx::tmem_wait_ld();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (C::P2 && rank != 0)
+              ptx::mbar_arrive_cluster(lead(&bars->s_free[sb]));
+            else
+              ptx::mbar_arrive(&bars->s_free[sb]);
+          }
+          float zc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int i = 0; i < PC; ++i) {
+            if constexpr (NORM == FS_NORM_SIGNED_L1)
+              zc[i & 3] = fma_abs_hi_lo<IN>(pw[i] & 0x7FFF7FFFu, zc[i & 3]);
+            else
+              zc[i & 3] = fma_sq_hi_lo<IN>(pw[i], zc[i & 3]);
+          }
+          za.x += (zc[0] + zc[1]) * inv_pz;
+          za.y += (zc[2] + zc[3]) * inv_pz;
         }
         if constexpr (DEFER_Z) {
           // the last chunk's a2(s) after P is handed over: off the P critical path (16-bit P: the

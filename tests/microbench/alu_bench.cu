@@ -60,6 +60,13 @@ __device__ __forceinline__ void step(float (&f)[CH], uint32_t (&u)[CH]) {
       asm volatile("fma.rn.f16x2 %0, %0, %0, %0;" : "+r"(u[i]));
     } else if constexpr (OP == 12) {  // IADD3-like int add
       asm volatile("add.u32 %0, %0, %1;" : "+r"(u[i]) : "r"(__float_as_uint(f[i])));
+    } else if constexpr (OP == 13) {  // FHFMA (fma.rn.f32.f16, mixed precision)
+      asm volatile("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tfma.rn.f32.f16 %0, lo, lo, %0;\n\t}" : "+f"(f[i]) : "r"(u[i]));
+    } else if constexpr (OP == 14) {  // F2FP + FHFMA x2 interleaved (convert then accumulate from the halves)
+      uint32_t h;
+      asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(f[i]), "f"(__uint_as_float(u[i])));
+      asm volatile("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tfma.rn.f32.f16 %0, lo, lo, %0;\n\tfma.rn.f32.f16 %0, hi, hi, %0;\n\t}" : "+f"(f[i]) : "r"(h));
+      u[i] ^= h;
     } else if constexpr (OP == 6) {  // F2F half2 via two scalar cvt (cvt.rn.f16.f32 x2 + pack)
       uint16_t lo, hi;
       asm volatile("cvt.rn.f16.f32 %0, %1;" : "=h"(lo) : "f"(f[i]));
@@ -94,21 +101,21 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 16);
   const char* names[] = {"cvt.f16x2", "cvt.bf16x2", "cvt.e4m3x2", "FFMA2", "FFMA", "FFMA2+cvt.f16x2", "2x cvt.f16",
-                         "cvt f16x2->e4m3x2", "PRMT", "FFMA2+PRMT", "FFMA2+cvt.e4m3x2", "HFMA2", "IADD"};
+                         "cvt f16x2->e4m3x2", "PRMT", "FFMA2+PRMT", "FFMA2+cvt.e4m3x2", "HFMA2", "IADD", "FHFMA", "F2FP+2xFHFMA"};
   const int iters = 4096;
-  for (int op = 0; op < 13; ++op) {
+  for (int op = 0; op < 15; ++op) {
     for (int w : {2, 4}) {
       const int threads = 128 * w;  // w warps per sub-partition
       void (*k)(int, unsigned long long*, float) = nullptr;
       switch (op) { case 0: k = bench<0>; break; case 1: k = bench<1>; break; case 2: k = bench<2>; break;
         case 3: k = bench<3>; break; case 4: k = bench<4>; break; case 5: k = bench<5>; break; case 6: k = bench<6>; break;
         case 7: k = bench<7>; break; case 8: k = bench<8>; break; case 9: k = bench<9>; break; case 10: k = bench<10>; break;
-        case 11: k = bench<11>; break; default: k = bench<12>; }
+        case 11: k = bench<11>; break; case 12: k = bench<12>; break; case 13: k = bench<13>; break; default: k = bench<14>; }
       k<<<1, threads>>>(64, d, 1.0f);
       k<<<1, threads>>>(iters, d, 1.0f);
       unsigned long long cyc = 0;
       cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-      const double instr_per_smsp = double(iters) * CH * w * (op == 5 || op == 6 || op == 9 || op == 10 ? 2 : 1);
+      const double instr_per_smsp = double(iters) * CH * w * (op == 5 || op == 6 || op == 9 || op == 10 ? 2 : op == 14 ? 3 : 1);
       printf("%-18s warps/SMSP %d: %.3f cycles per warp instr per SMSP\n", names[op], w, cyc / instr_per_smsp);
     }
   }
