@@ -258,12 +258,17 @@ __global__ void __launch_bounds__(128) gram_reduce_kernel(const float* __restric
   }
 }
 
-template <int D>
+// NT: B-image terms applied -- 2 (hi + lo, ~2^-16: float32 outputs) or 1 (hi only, one rounding of
+// the moments to the operand dtype, below a 16-bit output's own rounding); the smem the lo term
+// would take holds four Q buffers instead of two (HBM latency x bandwidth needs ~3 in flight)
+template <int D, int NT>
 struct ApplyCfg {
   static constexpr int Q_BYTES = BK * D * 2;
-  static constexpr int IMG_OFF = 2 * Q_BYTES;
-  static constexpr int BAR_OFF = IMG_OFF + ImgCfg<D>::BYTES;
-  static constexpr int SMEM = BAR_OFF + 1024 + 1024;
+  static constexpr int NQB = NT == 1 ? 4 : 2;
+  static constexpr int IMG_OFF = NQB * Q_BYTES;
+  static constexpr int IMG_BYTES = NT * ImgCfg<D>::TERM;
+  static constexpr int BAR_OFF = IMG_OFF + IMG_BYTES;
+  static constexpr int SMEM = BAR_OFF + 4096 + 1024;  // barriers + the epilogue's z exchange (2 KB)
   static constexpr int TN = 2 * D;  // accumulator columns per buffer
   static constexpr int TCOLS = 2 * TN;
 };
@@ -301,18 +306,19 @@ __device__ __forceinline__ void store8(void* dst, const float* v) {
 }
 
 // Launch 3: persistent; CTA i takes a contiguous range of (b, h, query tile) so the B image of a
-// (b, h_kv) is loaded once per run of tiles.  Warp 0: bulk / TMA loads; warp 1: MMAs; warps 2-5:
-// epilogue (warp w reads TMEM lane quarter w % 4).
+// (b, h_kv) is loaded once per run of tiles.  Warp 0: bulk / TMA loads; warp 1: MMAs; warps 2-9:
+// epilogue (warp w reads TMEM lane quarter w % 4, column half (w - 2) / 4).
 template <int IN, int D, int OUT>
-__global__ void __launch_bounds__(192, 1) gram_apply_kernel(const __grid_constant__ CUtensorMap tm_q, ApplyArgs a) {
-  using C = ApplyCfg<D>;
+__global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constant__ CUtensorMap tm_q, ApplyArgs a) {
+  constexpr int NT = 2;  // (1 -- hi only, four Q buffers -- measured no faster and outside bf16 tolerance)
+  using C = ApplyCfg<D, NT>;
   constexpr int NB = D / 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
-  uint64_t *q_full = bars, *q_empty = bars + 2, *t_full = bars + 4, *t_empty = bars + 6;
-  uint64_t *img_full = bars + 8, *img_empty = bars + 9;
-  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t *q_full = bars, *q_empty = bars + 4, *t_full = bars + 8, *t_empty = bars + 10;
+  uint64_t *img_full = bars + 12, *img_empty = bars + 13;
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 14);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int per = (a.n_tiles + gridDim.x - 1) / gridDim.x;
   const int tb0 = blockIdx.x * per, tb1 = min(a.n_tiles, tb0 + per);
@@ -322,11 +328,13 @@ __global__ void __launch_bounds__(192, 1) gram_apply_kernel(const __grid_constan
     return b * a.heads_kv + static_cast<int>((static_cast<int64_t>(h) * a.heads_kv) / a.heads_q);
   };
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NQB; ++i) {
       ptx::mbar_init(&q_full[i], 1);
-      ptx::mbar_init(&q_empty[i], 1 + 4);  // the MMAs' commit + the four epilogue warps (they read q)
+      ptx::mbar_init(&q_empty[i], 1 + 8);  // the MMAs' commit + the eight epilogue warps (they read q)
+    }
+    for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&t_full[i], 1);
-      ptx::mbar_init(&t_empty[i], 4);
+      ptx::mbar_init(&t_empty[i], 8);
     }
     ptx::mbar_init(img_full, 1);
     ptx::mbar_init(img_empty, 1);
@@ -346,15 +354,15 @@ __global__ void __launch_bounds__(192, 1) gram_apply_kernel(const __grid_constan
         const int kv = bhkv_of(tile);
         if (kv != cur) {
           if (n_img > 0) ptx::mbar_wait(img_empty, (n_img - 1) & 1u);
-          ptx::mbar_arrive_expect_tx(img_full, ImgCfg<D>::BYTES);
+          ptx::mbar_arrive_expect_tx(img_full, C::IMG_BYTES);
           const uint8_t* src = reinterpret_cast<const uint8_t*>(a.img) + static_cast<int64_t>(kv) * ImgCfg<D>::BYTES;
-          for (int off = 0; off < ImgCfg<D>::BYTES; off += 32768)
-            ptx::bulk_load(smem + C::IMG_OFF + off, src + off, min(32768, ImgCfg<D>::BYTES - off), img_full);
+          for (int off = 0; off < C::IMG_BYTES; off += 32768)
+            ptx::bulk_load(smem + C::IMG_OFF + off, src + off, min(32768, C::IMG_BYTES - off), img_full);
           cur = kv;
           ++n_img;
         }
-        const int qb = it & 1;
-        ptx::mbar_wait(&q_empty[qb], ((it >> 1) & 1u) ^ 1u);
+        const int qb = it % C::NQB;
+        ptx::mbar_wait(&q_empty[qb], ((it / C::NQB) & 1u) ^ 1u);
         ptx::mbar_arrive_expect_tx(&q_full[qb], C::Q_BYTES);
         const int bh = tile / a.n_qt, qt = tile % a.n_qt;
 #pragma unroll
@@ -374,14 +382,14 @@ __global__ void __launch_bounds__(192, 1) gram_apply_kernel(const __grid_constan
         cur = kv;
         ++n_img;
       }
-      const int qb = it & 1, tb = it & 1;
-      ptx::mbar_wait(&q_full[qb], (it >> 1) & 1u);
+      const int qb = it % C::NQB, tb = it & 1;
+      ptx::mbar_wait(&q_full[qb], (it / C::NQB) & 1u);
       ptx::mbar_wait(&t_empty[tb], ((it >> 1) & 1u) ^ 1u);
       ptx::tc_fence_after();
       const uint32_t qa = ptx::smem_u32(smem + qb * C::Q_BYTES);
       const uint32_t ia = ptx::smem_u32(smem + C::IMG_OFF);
 #pragma unroll
-      for (int term = 0; term < 2; ++term)
+      for (int term = 0; term < NT; ++term)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off_a = (ks * 32 / 128) * BLK + (ks * 32) % 128;
@@ -394,44 +402,77 @@ __global__ void __launch_bounds__(192, 1) gram_apply_kernel(const __grid_constan
       if (tile + 1 >= tb1 || bhkv_of(tile + 1) != kv) ptx::tc_commit_p(img_empty, lp);
     }
   } else {
-    // epilogue: thread = query row r of the tile
-    const int quarter = warp & 3;
+    // epilogue, 8 warps: warp w reads TMEM lane quarter w % 4 (rows r) and column half hf of both
+    // moments -- partial z over its half of G's columns, exchanged with its partner warp (same
+    // quarter, other half) through shared memory and a 64-thread named barrier, then its half of O
+    constexpr int HD = D / 2;     // columns per half
+    constexpr int NL = HD / 32;   // 32-column TMEM loads per half
+    const int quarter = warp & 3, hf = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    float* zx = reinterpret_cast<float*>(bars + 16);  // [2 tiles][2 halves][128 rows]
+    int cur_kv = -1;
+    float sW = 0.f, sG = 0.f;  // the moments' scales, loaded once per run of tiles of a (b, h_kv)
     for (int tile = tb0, it = 0; tile < tb1; ++tile, ++it) {
-      const int qb = it & 1, tb = it & 1;
+      const int qb = it % C::NQB, tb = it & 1;
       const int bh = tile / a.n_qt, qt = tile % a.n_qt;
       const int kv = bhkv_of(tile);
-      const float sW = a.scl[2 * kv], sG = a.scl[2 * kv + 1];
-      ptx::mbar_wait(&t_full[tb], (it >> 1) & 1u);
-      ptx::tc_fence_after();
-      // z = sum_a T^G_a q_a (q from the swizzled Q tile in shared memory)
+      if (kv != cur_kv) {  // (issued before the accumulator wait: the load latency hides behind it)
+        sW = a.scl[2 * kv];
+        sG = a.scl[2 * kv + 1];
+        cur_kv = kv;
+      }
+      // this row's half of q, straight from the swizzled Q tile as soon as it lands, so the Q buffer
+      // frees when the MMAs finish (not after the accumulator is drained): the producer can keep
+      // the next-but-one tile's load in flight
+      ptx::mbar_wait(&q_full[qb], (it / C::NQB) & 1u);
       const uint8_t* qrow = smem + qb * C::Q_BYTES + r * 128;
-      float zs = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t t[32];
-        ptx::tmem_ld32(tmem + lane_off + tb * C::TN + D + c * 32, t);
-        ptx::tmem_wait_ld();
+      uint4 qv[HD / 8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {  // 16-byte chunk (c*4 + j) of the row: 8 elements
-          const int chunk = c * 4 + j, kb = chunk >> 3, cj = chunk & 7;
-          const uint4 w = *reinterpret_cast<const uint4*>(qrow + kb * BLK + ((cj ^ (r & 7)) << 4));
-          const uint16_t* e = reinterpret_cast<const uint16_t*>(&w);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) zs = fmaf(__uint_as_float(t[j * 8 + u]), from16<IN>(e[u]), zs);
-        }
+      for (int j = 0; j < HD / 8; ++j) {  // 16-byte chunk of the row: 8 elements
+        const int chunk = hf * (HD / 8) + j, kb = chunk >> 3, cj = chunk & 7;
+        qv[j] = *reinterpret_cast<const uint4*>(qrow + kb * BLK + ((cj ^ (r & 7)) << 4));
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&q_empty[qb]);
+      ptx::mbar_wait(&t_full[tb], (it >> 1) & 1u);
+      ptx::tc_fence_after();
+      // partial z = sum over this half's columns a of T^G_a q_a
+      uint32_t t[NL][32];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) ptx::tmem_ld32(tmem + lane_off + tb * C::TN + D + hf * HD + l * 32, t[l]);
+      ptx::tmem_wait_ld();
+      float zs0 = 0.f, zs1 = 0.f;
+#pragma unroll
+      for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint16_t* e = reinterpret_cast<const uint16_t*>(&qv[l * 4 + j]);
+#pragma unroll
+          for (int u = 0; u < 8; u += 2) {
+            zs0 = fmaf(__uint_as_float(t[l][j * 8 + u]), from16<IN>(e[u]), zs0);
+            zs1 = fmaf(__uint_as_float(t[l][j * 8 + u + 1]), from16<IN>(e[u + 1]), zs1);
+          }
+        }
+      // T^W half in flight while the partial z is exchanged
+#pragma unroll
+      for (int l = 0; l < NL; ++l) ptx::tmem_ld32(tmem + lane_off + tb * C::TN + hf * HD + l * 32, t[l]);
+      float* zt = zx + (it & 1) * 256;
+      zt[hf * 128 + r] = zs0 + zs1;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      const float zsum = zt[r] + zt[128 + r];
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&t_empty[tb]);
       const int row = qt * BK + r;
       const bool live = row < a.seqlen_q;
       // the reference's z and denominator (normalizers.py:83-91); Gram rounding can leave a tiny
       // negative z where the exact one is 0
-      const float z = a.scale * a.scale * fmaxf(zs, 0.f) * sG;
+      const float z = a.scale * a.scale * fmaxf(zsum, 0.f) * sG;
       const float den = sqrtf(z + a.eps);
       const bool bad = !(den > 0.f) || isinf(den);
-      if (live && bad && a.bad_key != nullptr) {
+      if (hf == 0 && live && bad && a.bad_key != nullptr) {
         const uint64_t lin = static_cast<uint64_t>(bh) * a.seqlen_q + row;
         atomicMin(reinterpret_cast<unsigned long long*>(a.bad_key),
                   static_cast<unsigned long long>((lin << 32) | __float_as_uint(z)));
@@ -440,28 +481,19 @@ __global__ void __launch_bounds__(192, 1) gram_apply_kernel(const __grid_constan
       const int h = bh % a.heads_q, b = bh / a.heads_q;
       using OT = typename std::conditional<OUT == FS_F32, float,
                                            typename std::conditional<OUT == FS_BF16, __nv_bfloat16, __half>::type>::type;
-      OT* dst = reinterpret_cast<OT*>(a.o) + b * a.o_sb + static_cast<int64_t>(row) * a.o_sn + h * a.o_sh;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t t[32];
-        ptx::tmem_ld32(tmem + lane_off + tb * C::TN + c * 32, t);
-        ptx::tmem_wait_ld();
-        if (c == D / 32 - 1) {
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&t_empty[tb]);
-        }
-        if (live) {
+      OT* dst = reinterpret_cast<OT*>(a.o) + b * a.o_sb + static_cast<int64_t>(row) * a.o_sn + h * a.o_sh + hf * HD;
+      if (live) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            if (c * 32 + j * 8 < a.head_dim) {
+            if (hf * HD + l * 32 + j * 8 < a.head_dim) {
               float v[8];
 #pragma unroll
-              for (int u = 0; u < 8; ++u) v[u] = bad ? 0.f : __uint_as_float(t[j * 8 + u]) * mul;
-              store8<OUT>(dst + c * 32 + j * 8, v);
+              for (int u = 0; u < 8; ++u) v[u] = bad ? 0.f : __uint_as_float(t[l][j * 8 + u]) * mul;
+              store8<OUT>(dst + l * 32 + j * 8, v);
             }
           }
-        }
       }
     }
   }
@@ -560,8 +592,9 @@ static fs_status run(const fs_fwd_params* p, const Plan& pl, uint8_t* ws, cudaSt
     a.eps = p->eps;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms_now())));
     auto go = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ApplyCfg<D>::SMEM);
-      kern<<<grid, 192, ApplyCfg<D>::SMEM, stream>>>(tq, a);
+      const int sm = ApplyCfg<D, 2>::SMEM;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      kern<<<grid, 320, sm, stream>>>(tq, a);
     };
     switch (p->out_dtype) {
       case FS_F32: go(gram_apply_kernel<IN, D, FS_F32>); break;
