@@ -912,18 +912,19 @@ def _sweep_cases(n=None, seed=None):
     for i in range(n):
         dt = dts[i % 3]
         d = int(rng.choice([16, 32, 48, 64, 80, 96, 112, 128] if dt != torch.float8_e4m3fn else [16, 32, 64, 96, 128]))
-        hkv = int(rng.choice([1, 2, 3]))
+        hkv = int(rng.choice([1, 2, 3, 8]))
         h = hkv * int(rng.choice([1, 2, 4]))
         out.append(dict(dt=dt, b=int(rng.integers(1, 4)), nq=int(rng.integers(1, 700)), nkv=int(rng.integers(1, 900)),
                         h=h, hkv=hkv, d=d, norm=str(rng.choice(["spherical", "signed_l1"])),
                         ks=bool(rng.integers(0, 2)), splits=int(rng.choice([1, 1, 2, 3])),
                         scale=float(rng.choice([1.0, -0.5, 2.0])), eps=float(rng.choice([0.0, 1e-3])),
-                        out=[torch.float32, torch.bfloat16][int(rng.integers(0, 2))], seed=int(rng.integers(1 << 30))))
+                        out=[torch.float32, torch.bfloat16][int(rng.integers(0, 2))], seed=int(rng.integers(1 << 30)),
+                        tail=bool(rng.integers(0, 2))))
     return out
 
 
 @pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"{str(c['dt'])[6:]}-d{c['d']}-n{c['nq']}x{c['nkv']}-"
-                                                                f"h{c['h']}/{c['hkv']}-{c['norm']}-ks{int(c['ks'])}-s{c['splits']}")
+                                                                f"h{c['h']}/{c['hkv']}-{c['norm']}-ks{int(c['ks'])}-s{c['splits']}{'t' if c['tail'] else ''}")
 def test_random_feature_sweep(case):
     c = case
     g = torch.Generator(device="cuda").manual_seed(c["seed"])
@@ -932,8 +933,10 @@ def test_random_feature_sweep(case):
     v = torch.randn((c["b"], c["nkv"], c["hkv"], c["d"]), generator=g, device="cuda").to(c["dt"])
     m = torch.randint(0, 4, (c["b"], c["nkv"]), generator=g, device="cuda").float() if c["ks"] else None
     eps = c["eps"] if not c["ks"] else max(c["eps"], 1e-3)  # zero multiplicities can empty a row
+    # (split_tail: only the last partial wave's work tiles take the K/V split; with few tiles every
+    # tile is a tail tile, with > 74 cluster tiles whole-wave and tail tiles mix)
     o = fs().fwd(q, k, v, scale=c["scale"], eps=eps, out_dtype=c["out"], normalizer=c["norm"], key_scale=m,
-                 kv_splits=c["splits"], check=False)
+                 kv_splits=c["splits"], split_tail=c.get("tail", False), check=False)
     ref = exact_of(q, k, v, c["scale"], eps, c["norm"], m)
     got = o.float().cpu().numpy()
     finite = np.isfinite(ref).all(axis=-1)
