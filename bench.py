@@ -575,9 +575,13 @@ def run_ours(args, cfg):
         return partition.fwd_shard(q, k, v, o, lo - u_off, hi - u_off,
                                    lambda *a, **k2: flashsign.fwd_async(*a, bad_key=bad, **k2), key_scale=mult, **kw)
 
-    n_launch_per_step = len(partition.pieces(q.shape[0], HKV, lo - u_off, hi - u_off))
-    # (--fused-mult, 16-bit: each piece is the K' = m K pass + the FlashSign kernel)
+    pcs = partition.pieces(q.shape[0], HKV, lo - u_off, hi - u_off)
+    n_launch_per_step = len(pcs)
+    # kernels per step besides the FlashSign kernels: the K' = m K pass per piece (--fused-mult,
+    # 16-bit) and the merge kernel of any piece whose automatic plan splits K/V (e.g. C3's tail wave)
     n_prepass = n_launch_per_step if (mult is not None and q.dtype in (torch.bfloat16, torch.float16)) else 0
+    n_merge = sum(1 for pc in pcs if flashsign.plan(pc.b1 - pc.b0, (pc.g1 - pc.g0) * r, N, N, dev, D,
+                                                    q.dtype).splits > 1)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -737,7 +741,7 @@ def run_ours(args, cfg):
                        "seq_len": N, "head_dim": D, "eps": cfg["eps"], "parallelism": f"batchxhead-shard{world}",
                        "l2": "inputs larger than L2 (no flush needed)",
                        "flops_per_step": total_flops},
-            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": (n_launch_per_step + n_prepass) * args.steps,
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": (n_launch_per_step + n_prepass + n_merge) * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "gather": gather,
             "e2e_dropin": e2e_dropin, "host_latency": lat,
         }

@@ -10,8 +10,8 @@
 // or deleting a zero-score key leaves the output bit-identical, as in the reference).
 //
 // CTA = (b, h, 64 query rows), 256 threads; K / V stream through shared memory in 32-key tiles:
-//   phase 1: S = Q K^T (thread: one row x 8 keys, float64 dot products), reference rounding
-//   phase 2: o += s v_j for every key in order (thread: one row x d/4 columns), z likewise
+//   phase 1: S = Q K^T (thread: 2 rows x 4 keys, float64 dot products), reference rounding
+//   phase 2: o += s v_j for every key in order (thread: 2 rows x d/8 columns), z likewise
 // Epilogue: b(z + eps), the first-bad-row key of fs_fwd (packed (linear row << 32) | float bits),
 // per-row z in float64 for the exception text, O in float64.
 
@@ -34,12 +34,18 @@ constexpr int THREADS = 256;
 
 template <int D, int NORM, bool F32>
 __global__ void __launch_bounds__(THREADS) exact_kernel(fs_exact_params p) {
-  constexpr int DP = D + 1;  // padded row stride (doubles): rows land in different banks
+  // Register-blocked: thread t owns rows {t/8, t/8 + 32} of the CTA's 64 and, in phase 1, keys
+  // {t%8 + 8u} of the tile (2 x 4 scores), in phase 2 columns {2 (t%8) + 16 w, + 1} (2 x D/8
+  // accumulators).  Rows are padded to D + 2 doubles so 16-byte loads of eight different keys
+  // (or columns) land in different banks.
+  constexpr int DP = D + 2;
+  constexpr int SP = BC + 1;
+  constexpr int NW = D / 16;  // column pairs per thread
   extern __shared__ double sm[];
   double* qs = sm;                 // [BR][DP]
   double* ks = qs + BR * DP;       // [BC][DP]
   double* vs = ks + BC * DP;       // [BC][DP]
-  double* ss = vs + BC * DP;       // [BR][BC + 1] scores after the reference's rounding
+  double* ss = vs + BC * DP;       // [BR][SP] scores after the reference's rounding
   const int tid = threadIdx.x;
   const int n_rb = (p.seqlen_q + BR - 1) / BR;
   const int rb = blockIdx.x % n_rb;
@@ -53,12 +59,13 @@ __global__ void __launch_bounds__(THREADS) exact_kernel(fs_exact_params p) {
     const int n = r0 + r;
     qs[r * DP + a] = (n < p.seqlen_q && a < d) ? p.q[b * p.q_stride[0] + n * p.q_stride[1] + h * p.q_stride[2] + a] : 0.0;
   }
-  const int row = tid >> 2, sub = tid & 3;  // phase 1 / 2 ownership: 4 threads per row
-  constexpr int NW = D / 4;
-  double o[NW];
+  const int rg = tid >> 3, kg = tid & 7;
+  double o[2][2 * NW];
 #pragma unroll
-  for (int w = 0; w < NW; ++w) o[w] = 0.0;
-  double z = 0.0;
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int w = 0; w < 2 * NW; ++w) o[i][w] = 0.0;
+  double z[2] = {0.0, 0.0};
   const double scale = p.scale;
   const float scale_f = static_cast<float>(p.scale);
   for (int c0 = 0; c0 < p.seqlen_kv; c0 += BC) {
@@ -73,57 +80,81 @@ __global__ void __launch_bounds__(THREADS) exact_kernel(fs_exact_params p) {
       vs[c * DP + a] = ok ? p.v[offv] : 0.0;
     }
     __syncthreads();
-    // phase 1: keys sub, sub + 4, ... of this tile for `row`
+    // phase 1: the 2 x 4 score block
+    {
+      double acc[2][4] = {};
+#pragma unroll 4
+      for (int a = 0; a < D; a += 2) {
+        const double2 q0 = *reinterpret_cast<const double2*>(qs + rg * DP + a);
+        const double2 q1 = *reinterpret_cast<const double2*>(qs + (rg + 32) * DP + a);
 #pragma unroll
-    for (int u = 0; u < BC / 4; ++u) {
-      const int c = sub + 4 * u;
-      double s = 0.0;
-#pragma unroll 8
-      for (int a = 0; a < D; ++a) s = fma(qs[row * DP + a], ks[c * DP + a], s);
-      if constexpr (F32) {
-        float sf = static_cast<float>(s);
-        if (scale != 1.0) sf *= scale_f;
-        s = static_cast<double>(sf);
-      } else if (scale != 1.0) {
-        s *= scale;
+        for (int u = 0; u < 4; ++u) {
+          const double2 kv = *reinterpret_cast<const double2*>(ks + (kg + 8 * u) * DP + a);
+          acc[0][u] = fma(q0.y, kv.y, fma(q0.x, kv.x, acc[0][u]));
+          acc[1][u] = fma(q1.y, kv.y, fma(q1.x, kv.x, acc[1][u]));
+        }
       }
-      ss[row * (BC + 1) + c] = s;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double sv = acc[i][u];
+          if constexpr (F32) {
+            float sf = static_cast<float>(sv);
+            if (scale != 1.0) sf *= scale_f;
+            sv = static_cast<double>(sf);
+          } else if (scale != 1.0) {
+            sv *= scale;
+          }
+          ss[(rg + 32 * i) * SP + kg + 8 * u] = sv;
+        }
     }
     __syncthreads();
     // phase 2: every key of the tile in order
     for (int c = 0; c < nc; ++c) {
-      const double s = ss[row * (BC + 1) + c];
-      double a2;
-      if constexpr (NORM == FS_NORM_SIGNED_L1) {
-        a2 = fabs(s);
-      } else if constexpr (F32) {
-        const float sf = static_cast<float>(s);
-        a2 = static_cast<double>(sf * sf);  // the float32 grid squares in float32
-      } else {
-        a2 = s * s;
-      }
-      z += a2;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) o[w] = fma(s, vs[c * DP + sub + 4 * w], o[w]);
+      for (int i = 0; i < 2; ++i) {
+        const double sv = ss[(rg + 32 * i) * SP + c];
+        double a2;
+        if constexpr (NORM == FS_NORM_SIGNED_L1) {
+          a2 = fabs(sv);
+        } else if constexpr (F32) {
+          const float sf = static_cast<float>(sv);
+          a2 = static_cast<double>(sf * sf);  // the float32 grid squares in float32
+        } else {
+          a2 = sv * sv;
+        }
+        z[i] += a2;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const double2 vv = *reinterpret_cast<const double2*>(vs + c * DP + 2 * kg + 16 * w);
+          o[i][2 * w] = fma(sv, vv.x, o[i][2 * w]);
+          o[i][2 * w + 1] = fma(sv, vv.y, o[i][2 * w + 1]);
+        }
+      }
     }
   }
-  const int n = r0 + row;
-  if (n >= p.seqlen_q) return;
-  const double zz = p.eps != 0.0 ? z + p.eps : z;
-  const double den = NORM == FS_NORM_SIGNED_L1 ? zz : sqrt(zz);
-  const bool bad = !(den != 0.0) || !isfinite(den);
-  const uint64_t lin = static_cast<uint64_t>(bh) * p.seqlen_q + n;
-  if (sub == 0) {
-    if (p.z_out) p.z_out[lin] = z;
-    if (bad && p.bad_key)
-      atomicMin(reinterpret_cast<unsigned long long*>(p.bad_key),
-                static_cast<unsigned long long>((lin << 32) | __float_as_uint(static_cast<float>(z))));
-  }
-  double* dst = p.o + b * p.o_stride[0] + static_cast<int64_t>(n) * p.o_stride[1] + h * p.o_stride[2];
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    const int a = sub + 4 * w;
-    if (a < d) dst[a] = o[w] / den;
+  for (int i = 0; i < 2; ++i) {
+    const int n = r0 + rg + 32 * i;
+    if (n >= p.seqlen_q) continue;
+    const double zz = p.eps != 0.0 ? z[i] + p.eps : z[i];
+    const double den = NORM == FS_NORM_SIGNED_L1 ? zz : sqrt(zz);
+    const bool bad = !(den != 0.0) || !isfinite(den);
+    const uint64_t lin = static_cast<uint64_t>(bh) * p.seqlen_q + n;
+    if (kg == 0) {
+      if (p.z_out) p.z_out[lin] = z[i];
+      if (bad && p.bad_key)
+        atomicMin(reinterpret_cast<unsigned long long*>(p.bad_key),
+                  static_cast<unsigned long long>((lin << 32) | __float_as_uint(static_cast<float>(z[i]))));
+    }
+    double* dst = p.o + b * p.o_stride[0] + static_cast<int64_t>(n) * p.o_stride[1] + h * p.o_stride[2];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int a = 2 * kg + 16 * w;
+      if (a < d) dst[a] = o[i][2 * w] / den;
+      if (a + 1 < d) dst[a + 1] = o[i][2 * w + 1] / den;
+    }
   }
 }
 
@@ -155,7 +186,7 @@ extern "C" fs_status fs_exact_fwd(const fs_exact_params* p, fs_stream_t stream_)
   const int64_t blocks = static_cast<int64_t>((p->seqlen_q + BR - 1) / BR) * p->heads_q * p->batch;
   if (blocks > INT32_MAX) return fail(FS_ERR_UNSUPPORTED, "too many query blocks");
   auto go = [&](auto kern, int d) {
-    const size_t smem = sizeof(double) * (static_cast<size_t>(BR + 2 * BC) * (d + 1) + BR * (BC + 1));
+    const size_t smem = sizeof(double) * (static_cast<size_t>(BR + 2 * BC) * (d + 2) + BR * (BC + 1));
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<static_cast<unsigned>(blocks), THREADS, smem, stream>>>(*p);
   };
