@@ -159,6 +159,35 @@ def test_sharded_equals_full_bitwise():
         assert torch.equal(o, full), world
 
 
+def test_sharded_c2_with_tail_split():
+    # 8-way batch x head shards of C2 (B16 H16 N4096 d64 fp16): each shard's launch is 256 work tiles
+    # = 3 waves + 34, so the automatic plan splits the tail wave's K/V (fs_plan, split_tail); the
+    # single full launch does not.  Rows of whole-wave tiles are bitwise the full launch's; tail rows
+    # differ only by the fp32 summation order of the two halves (one fp16 rounding at most).
+    # With kv_splits=1 every shard is bitwise the full launch.
+    from paper_2505_09326_b200 import partition
+    B, N, H, D = 16, 4096, 16, 64
+    q = rand_bshd(B, N, H, D, torch.float16, 25)
+    k = rand_bshd(B, N, H, D, torch.float16, 26)
+    v = rand_bshd(B, N, H, D, torch.float16, 27)
+    full = fs().fwd(q, k, v)
+    lo, hi = partition.unit_range(B * H, 8, 0)
+    pl = fs().plan(2, H, N, N, q.device, D, torch.float16)
+    assert pl.split_tail == 1 and pl.splits == 2 and pl.efficiency > 0.98
+    for splits, exact in ((None, False), (1, True)):
+        o = torch.full_like(full, float("nan"))
+        for rank in range(8):
+            lo, hi = partition.unit_range(B * H, 8, rank)
+            partition.fwd_shard(q, k, v, o, lo, hi, fs().fwd_async, kv_splits=splits)
+        if exact:
+            assert torch.equal(o, full)
+        else:
+            d = (o.float() - full.float()).abs()
+            assert bool(torch.isfinite(o).all())
+            assert float(d.max()) <= 2.0 ** -10 * max(1.0, float(full.float().abs().max()))
+            assert float((d == 0).float().mean()) >= 0.9
+
+
 def test_negating_k_single_key_flips_exactly():
     # test_attention.py:186-191
     q = rand_bshd(1, 6, 1, 64, torch.bfloat16, 22)
