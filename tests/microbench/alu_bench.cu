@@ -67,6 +67,10 @@ __device__ __forceinline__ void step(float (&f)[CH], uint32_t (&u)[CH]) {
       asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(f[i]), "f"(__uint_as_float(u[i])));
       asm volatile("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tfma.rn.f32.f16 %0, lo, lo, %0;\n\tfma.rn.f32.f16 %0, hi, hi, %0;\n\t}" : "+f"(f[i]) : "r"(h));
       u[i] ^= h;
+    } else if constexpr (OP == 15) {  // cvt.rs e4m3x4 (stochastic rounding, 4 values per instr)
+      uint32_t r;
+      asm volatile("cvt.rs.satfinite.e4m3x4.f32 %0, {%1, %2, %3, %4}, %5;" : "=r"(r) : "f"(f[i]), "f"(__uint_as_float(u[i])), "f"(f[i]), "f"(__uint_as_float(u[i])), "r"(0x80808080u));
+      u[i] ^= r;
     } else if constexpr (OP == 6) {  // F2F half2 via two scalar cvt (cvt.rn.f16.f32 x2 + pack)
       uint16_t lo, hi;
       asm volatile("cvt.rn.f16.f32 %0, %1;" : "=h"(lo) : "f"(f[i]));
@@ -101,16 +105,16 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 16);
   const char* names[] = {"cvt.f16x2", "cvt.bf16x2", "cvt.e4m3x2", "FFMA2", "FFMA", "FFMA2+cvt.f16x2", "2x cvt.f16",
-                         "cvt f16x2->e4m3x2", "PRMT", "FFMA2+PRMT", "FFMA2+cvt.e4m3x2", "HFMA2", "IADD", "FHFMA", "F2FP+2xFHFMA"};
+                         "cvt f16x2->e4m3x2", "PRMT", "FFMA2+PRMT", "FFMA2+cvt.e4m3x2", "HFMA2", "IADD", "FHFMA", "F2FP+2xFHFMA", "cvt.rs.e4m3x4"};
   const int iters = 4096;
-  for (int op = 0; op < 15; ++op) {
+  for (int op = 0; op < 16; ++op) {
     for (int w : {2, 4}) {
       const int threads = 128 * w;  // w warps per sub-partition
       void (*k)(int, unsigned long long*, float) = nullptr;
       switch (op) { case 0: k = bench<0>; break; case 1: k = bench<1>; break; case 2: k = bench<2>; break;
         case 3: k = bench<3>; break; case 4: k = bench<4>; break; case 5: k = bench<5>; break; case 6: k = bench<6>; break;
         case 7: k = bench<7>; break; case 8: k = bench<8>; break; case 9: k = bench<9>; break; case 10: k = bench<10>; break;
-        case 11: k = bench<11>; break; case 12: k = bench<12>; break; case 13: k = bench<13>; break; default: k = bench<14>; }
+        case 11: k = bench<11>; break; case 12: k = bench<12>; break; case 13: k = bench<13>; break; case 14: k = bench<14>; break; default: k = bench<15>; }
       k<<<1, threads>>>(64, d, 1.0f);
       k<<<1, threads>>>(iters, d, 1.0f);
       unsigned long long cyc = 0;

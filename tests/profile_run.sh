@@ -23,6 +23,12 @@ done
 for c in $FULL; do
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:flashsign_fwd -s 3 -c 1 -o $OUT/prof_$c \
   python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-cpu --no-context > $OUT/ncu_$c.log 2>&1
+# summaries on the box (the .ncu-rep files are ~20 MB each; gpurun copies back <= 64 MiB)
+ncu -i $OUT/prof_$c.ncu-rep --page details --csv > $OUT/ncu_full_${c}_details.csv 2>/dev/null
+ncu -i $OUT/prof_$c.ncu-rep --page source --csv --print-source sass > $OUT/src_$c.csv 2>/dev/null
+python tests/ncu_hot.py $OUT/src_$c.csv 40 > $OUT/ncu_full_${c}_hot_sass.txt 2>&1
+rm -f $OUT/src_$c.csv
+[ "$c" = "c3" ] || rm -f $OUT/prof_$c.ncu-rep
 done
 tail -2 $OUT/ncu_c3.log
 ls -la $OUT
