@@ -271,6 +271,34 @@ def test_auto_splits_wave_model():
     assert plan(16, 16, 4096, 64, _lib.FS_F16).splits == 1   # C2 on one GPU: 27.7 waves, a split would not pay
 
 
+def test_plan_edge_cases():
+    # host-only fs_plan: empty launches, short K/V streams, partial_only (context parallelism wants
+    # every row's partial: never a tail split), explicit split_tail, whole waves (nothing to balance)
+    def params(b, h, nq, nkv, d=128):
+        p = _params(head_dim=d, seqlen_kv=nkv, seqlen_q=nq, batch=b, heads_q=h, heads_kv=h)
+        p.in_dtype = _lib.FS_BF16
+        return p
+    p = params(0, 4, 256, 256)
+    p.kv_splits = _lib.FS_SPLITS_AUTO
+    assert _lib.plan(p, 74).splits == 1 and _lib.plan(p, 74).items == 0
+    p = params(1, 80, 1024, 4096)                      # 160 tiles = 2 waves + 12
+    p.kv_splits = _lib.FS_SPLITS_AUTO
+    auto = _lib.plan(p, 74)
+    assert auto.split_tail == 1 and auto.n_whole == 148 and auto.tail_tiles == 12
+    assert auto.partial_floats == auto.splits * 12 * 512 * 129
+    p.partial_only = 1
+    cp = _lib.plan(p, 74)
+    assert cp.split_tail == 0 and cp.splits == 1
+    p.partial_only, p.kv_splits, p.split_tail = 0, 3, 1
+    ex = _lib.plan(p, 74)
+    assert (ex.splits, ex.split_tail, ex.items) == (3, 1, 148 + 36)
+    ex80 = _lib.plan(p, 80)                            # 160 = 2 whole waves of 80: no tail to split
+    assert (ex80.splits, ex80.split_tail, ex80.items) == (1, 0, 160)
+    p.kv_splits = -2
+    with pytest.raises(ValueError):
+        _lib.plan(p, 74)
+
+
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 def test_wave_efficiency_of_sharded_configs(world):
     # batch x head shards of C2-C5 (BASELINE.json configs) on `world` GPUs: each rank's launch
