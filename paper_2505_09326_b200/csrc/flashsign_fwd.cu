@@ -129,6 +129,9 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_EXP_NOZ
 #define FS_EXP_NOZ 0  // experiment (wrong results): skip the norm warps' a2(s) accumulation
 #endif
+#ifndef FS_F16ACC
+#define FS_F16ACC 0  // experiment (measured slower): fp16 QK accumulation, S is P (Cfg HA)
+#endif
 #ifndef FS_ZP
 // 16-bit inputs: z = sum a2(p) over the packed P the PV MMA reads, accumulated after P is handed
 // over (mixed-precision FHFMA straight from the packed halves, re-read from TMEM), so the norm
@@ -246,7 +249,7 @@ struct InTraits<FS_E4M3> {
   static constexpr float PMAX = 432.0f;
 };
 
-template <int IN, int D, bool KS = false>
+template <int IN, int D, bool KS = false, bool HA = false>
 struct Cfg {
   using TR = InTraits<IN>;
   static constexpr int EB = TR::EB;
@@ -321,7 +324,10 @@ struct Cfg {
   static_assert(NSB * BN + NOB * NQT * D <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
   static_assert(PV_STEPS % 2 == 0, "P is produced in two column halves");
-  static constexpr uint32_t IDESC_QK = ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, MMA_M, BN);
+  // HA (fp16 inputs): QK accumulates in fp16, so S is already P's type; tcgen05 writes a 16-bit D
+  // one element per 32-bit column, and tcgen05.ld .pack::16b hands two adjacent ones over packed
+  static constexpr uint32_t IDESC_QK =
+      ptx::idesc_make(TR::FMT, TR::FMT, 0, 0, MMA_M, BN) & ~(HA ? (3u << 4) : 0u);
   static constexpr uint32_t IDESC_PV = ptx::idesc_make(TR::FMT, TR::FMT, 0, 1, MMA_M, D);
 };
 
@@ -464,12 +470,13 @@ __device__ __forceinline__ TileCoord decode_tile(int tile, const KParams& p, int
 // NORM: FS_NORM_SPHERICAL (a2 = s^2, b = sqrt) | FS_NORM_SIGNED_L1 (a2 = |s|, b = id), normalizers.py:94-117.
 // KS: per-key multiplicity scale m_j fused into the score (s_ij -> m_j s_ij), attention.py:381-388.
 // PEER: partials stored into the owning rank's workspace over peer memory (fs_fwd_peer).
-template <int IN, int D, int OUT, int NORM, bool KS, bool PEER>
+template <int IN, int D, int OUT, int NORM, bool KS, bool PEER, bool HA = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     flashsign_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_m,
                          const KParams p) {
-  using C = Cfg<IN, D, KS>;
+  using C = Cfg<IN, D, KS, HA>;
+  static_assert(!HA || (IN == FS_F16 && !KS), "fp16 accumulation: fp16 inputs, no per-score multiplicities");
   using TR = InTraits<IN>;
   constexpr int BN = C::BN;  // keys per K/V tile for this configuration
   extern __shared__ uint8_t smem_raw[];
@@ -949,6 +956,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int hi = 0; hi < NH; ++hi) {
         const int hh = hh0 + hi;
         const uint32_t s_addr = s_base + hh * (BN / 2);
+        if constexpr (HA) {
+          // fp16 S straight from the MMA: packed pairs by the TMEM load path (no conversion),
+          // stored as P over the half's first columns once every chunk is in registers; z from
+          // the same packed values after P is handed over (FHFMA), off the critical path
+          constexpr int NCH = BN / 64;
+          uint32_t pk[NCH][16];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) ptx::tmem_ld16_pack(s_addr + 32 * ch, pk[ch]);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) ptx::tmem_st16(s_addr + 16 * ch, pk[ch]);
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (C::P2 && rank != 0)
+              ptx::mbar_arrive_cluster(lead(&bars->p_full[sb]));
+            else
+              ptx::mbar_arrive(&bars->p_full[sb]);
+          }
+          float zc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if constexpr (NORM == FS_NORM_SIGNED_L1)
+                zc[i & 3] = fma_abs_hi_lo<IN>(pk[ch][i] & 0x7FFF7FFFu, zc[i & 3]);
+              else
+                zc[i & 3] = fma_sq_hi_lo<IN>(pk[ch][i], zc[i & 3]);
+            }
+          za.x += zc[0] + zc[1];
+          za.y += zc[2] + zc[3];
+#if FS_PROF
+          pr_nc += clock64() - tn1;
+          ++pr_nn;
+#endif
+          continue;
+        }
         // BN/2 columns in 32-column chunks (80 registers/thread at 768 threads): the next chunk's
         // TMEM load is issued once this chunk is packed, and overlaps this chunk's P store.
         constexpr int NCH = BN / 64;
@@ -1759,10 +1804,10 @@ static fs_status combine_peer(const fs_fwd_params* p, const fs_peer_params* pp, 
   return FS_OK;
 }
 
-template <int IN, int D, int OUT, int NORM, bool KS, bool PEER = false>
+template <int IN, int D, int OUT, int NORM, bool KS, bool PEER = false, bool HA = false>
 static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
-  using C = Cfg<IN, D, KS>;
-  auto kern = flashsign_fwd_kernel<IN, D, OUT, NORM, KS, PEER>;
+  using C = Cfg<IN, D, KS, HA>;
+  auto kern = flashsign_fwd_kernel<IN, D, OUT, NORM, KS, PEER, HA>;
   // the >48 KB dynamic shared-memory opt-in is per device (context): set it once per device
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
@@ -1875,6 +1920,23 @@ static fs_status launch(const fs_fwd_params* p, cudaStream_t stream) {
 
 template <int IN, int D, int NORM, bool KS>
 static fs_status dispatch_out(const fs_fwd_params* p, cudaStream_t s) {
+  // fp16 inputs at p_scale 1 (no device scales, no per-score multiplicities): fp16 QK accumulation
+  // (Cfg HA; `FS_F16ACC`), S is P without a conversion pass
+  constexpr bool HA_OK = FS_F16ACC && IN == FS_F16 && !KS;
+  if constexpr (HA_OK) {
+    if (p->p_scale == 1.0f && p->dev_scales == nullptr) {
+      switch (p->out_dtype) {
+        case FS_F32:
+          return launch<IN, D, FS_F32, NORM, KS, false, true>(p, s);
+        case FS_BF16:
+          return launch<IN, D, FS_BF16, NORM, KS, false, true>(p, s);
+        case FS_F16:
+          return launch<IN, D, FS_F16, NORM, KS, false, true>(p, s);
+        default:
+          return fail(FS_ERR_DTYPE, "out_dtype must be FS_F32, FS_BF16 or FS_F16");
+      }
+    }
+  }
   switch (p->out_dtype) {
     case FS_F32:
       return launch<IN, D, FS_F32, NORM, KS>(p, s);

@@ -43,6 +43,14 @@ __global__ void k(uint32_t* out) {
     tmem_ld32(tm + (0u << 16), r);
     tmem_wait_ld();
     if (threadIdx.x == 5) for (int i = 0; i < 32; ++i) out[i] = r[i];
+    uint32_t q[16];  // the same 32 columns, two 16-bit elements per register (pack::16b)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 "
+                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
+                   "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
+                 : "r"(tm) : "memory");
+    tmem_wait_ld();
+    if (threadIdx.x == 5) for (int i = 0; i < 16; ++i) out[32 + i] = q[i];
   }
   tc_fence_before();
   __syncthreads();
@@ -50,19 +58,22 @@ __global__ void k(uint32_t* out) {
 }
 
 int main() {
-  uint32_t* d; cudaMalloc(&d, 128);
-  uint32_t h[32];
+  uint32_t* d; cudaMalloc(&d, 256);
+  uint32_t h[48];
   for (int f = 0; f < 2; ++f) {
     if (f == 0) { cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000); k<1><<<1, 128, 60000>>>(d); }
     else { cudaFuncSetAttribute(k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000); k<0><<<1, 128, 60000>>>(d); }
     cudaError_t e = cudaDeviceSynchronize();
-    cudaMemcpy(h, d, 128, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, d, 192, cudaMemcpyDeviceToHost);
     printf("%s (%s): ", f == 0 ? "F32 acc" : "F16 acc", cudaGetErrorString(e));
     for (int i = 0; i < 8; ++i) {
       if (f == 0) printf("%g ", *reinterpret_cast<float*>(&h[i]));
       else { __half lo = *reinterpret_cast<__half*>(&h[i]); __half hi = *(reinterpret_cast<__half*>(&h[i]) + 1);
              printf("[%g|%g] ", __half2float(lo), __half2float(hi)); }
     }
+    printf("\n   pack::16b: ");
+    for (int i = 32; i < 36; ++i) { __half lo = *reinterpret_cast<__half*>(&h[i]); __half hi = *(reinterpret_cast<__half*>(&h[i]) + 1);
+                                     printf("[%g|%g] ", __half2float(lo), __half2float(hi)); }
     printf("\n");
   }
   return 0;
