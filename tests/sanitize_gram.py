@@ -16,3 +16,15 @@ for dt in (torch.bfloat16, torch.float16):
         fs.gram_fwd(q, k, v, out_dtype=torch.float32, check=False)
 torch.cuda.synchronize()
 print("sanitize_gram ok")
+# the float64 mode kernel (fs_exact_fwd) through the drop-in API
+import numpy as np  # noqa: E402
+
+from paper_2505_09326_b200 import SPHERICAL, attention  # noqa: E402
+
+attention.set_compute_dtype("f64")
+rng = np.random.default_rng(3)
+for (y, x, d) in ((70, 100, 32), (130, 70, 64), (65, 33, 128)):
+    q, k, v = (rng.standard_normal((n, d)).astype(np.float32) for n in (y, x, x))
+    attention.streamed_attention_array(q, k, v, SPHERICAL, 0.5, attention.TileConfig())
+torch.cuda.synchronize()
+print("sanitize_exact ok")
