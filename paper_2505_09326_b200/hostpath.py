@@ -6,9 +6,12 @@ hand over float32 / float64 (or float16) numpy arrays and expect the reference's
 result dtype back.  Per call, on three CUDA streams of the current device:
 
   copy-in   K and V, then Q in row chunks, cross the host link in the caller's own dtype
-            (no host-side conversion pass); pageable source memory is copied directly
-            (``FLASHSIGN_H2D=pageable``, default) or through a pinned ring filled by host
-            threads (``staged``)
+            (no host-side conversion pass); arrays of >= 8 MB go through a pinned ring that host
+            threads fill while the DMA engine drains the previous slot (pinned DMA runs ~5x the
+            pageable rate; C3 through the reference's call pattern 54 -> ~115 TFLOP/s, bound
+            by the host-side copy at ~20 GB/s), smaller ones
+            are copied from pageable memory directly (``FLASHSIGN_H2D=auto``, default;
+            ``pageable`` / ``staged`` force one)
   compute   ``fs_prepare`` converts each tensor on the device to the kernel's operand
             dtype with one power-of-two scale per tensor and a Cauchy-Schwarz P scale
             (include/flashsign.h), so no finite input the reference accepts can overflow
@@ -35,6 +38,9 @@ from . import flashsign
 _SRC_TORCH = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
               np.dtype(np.float16): torch.float16}
 _CHUNK_BYTES = int(os.environ.get("FLASHSIGN_CHUNK_MB", "32")) << 20
+_STAGE_MIN_BYTES = 8 << 20  # auto mode: pinned staging from this size on
+# pinned ring slot: 64 MB measured best for the host-thread fill (C3 drop-in 95 -> 116 TFLOP/s vs 32 MB)
+_STAGE_BYTES = int(os.environ.get("FLASHSIGN_STAGE_MB", "64")) << 20
 
 
 class _Engine:
@@ -49,7 +55,7 @@ class _Engine:
             self.stats = torch.zeros(6, dtype=torch.float64, device=dev)
             self.scales = torch.ones(4, dtype=torch.float32, device=dev)
         self.lock = threading.Lock()  # one call at a time per device (shared workspaces)
-        self.mode = os.environ.get("FLASHSIGN_H2D", "pageable")
+        self.mode = os.environ.get("FLASHSIGN_H2D", "auto")
         self.pool = None
         self.ring = []
 
@@ -58,7 +64,7 @@ class _Engine:
         """Copy the contiguous host array ``src`` into ``dst`` on the copy-in stream."""
         if src.size == 0:
             return
-        if self.mode != "staged":
+        if self.mode == "pageable" or (self.mode == "auto" and src.nbytes < _STAGE_MIN_BYTES):
             with torch.cuda.stream(self.s_h2d):
                 dst.copy_(torch.from_numpy(src).view(dst.shape), non_blocking=True)
             return
@@ -66,12 +72,13 @@ class _Engine:
         flat_src = src.reshape(-1).view(np.uint8)
         flat_dst = dst.view(-1).view(torch.uint8)
         if not self.ring:
-            self.pool = ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1)))
-            self.ring = [(torch.empty(_CHUNK_BYTES, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+            self.pool = ThreadPoolExecutor(int(os.environ.get("FLASHSIGN_H2D_THREADS", 0))
+                                           or max(1, min(8, os.cpu_count() or 1)))
+            self.ring = [(torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
                          for _ in range(3)]
         nthr = self.pool._max_workers
-        for i, lo in enumerate(range(0, flat_src.size, _CHUNK_BYTES)):
-            hi = min(lo + _CHUNK_BYTES, flat_src.size)
+        for i, lo in enumerate(range(0, flat_src.size, _STAGE_BYTES)):
+            hi = min(lo + _STAGE_BYTES, flat_src.size)
             buf, ev = self.ring[i % len(self.ring)]
             ev.synchronize()  # the DMA that last read this slot is done
             host = buf.numpy()[:hi - lo]
