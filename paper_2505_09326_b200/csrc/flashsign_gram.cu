@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -47,6 +48,7 @@ void set_last_error(const char* msg);
 namespace gram {
 
 constexpr int BK = 128;             // keys per K/V tile (launch 1) = query rows per tile (launch 3)
+constexpr int kGramPrefetch = 0;    // apply kernel: L2 prefetch distance of Q tiles (FLASHSIGN_GRAM_PF)
 constexpr int BLK = BK * 128;       // one SW128 column block: 128 rows x 64 16-bit elements
 
 template <int D>
@@ -281,6 +283,7 @@ struct ApplyArgs {
   uint64_t* bad_key;
   int heads_q, heads_kv, seqlen_q, head_dim, n_qt, n_tiles;
   float scale, eps;
+  int pf;  // L2 prefetch distance for Q tiles (0: off)
 };
 
 template <int OUT>
@@ -362,6 +365,17 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
           ++n_img;
         }
         const int qb = it % C::NQB;
+        if (a.pf > 0) {
+          // two Q buffers hold ~64 KB in flight per SM; the HBM latency x bandwidth product needs
+          // ~160 KB: the tile `pf` ahead is pulled into L2 (each tile once), so its TMA load hits L2
+          const int tp = tile + a.pf;
+          if (tp < tb1) {
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+              ptx::tma_prefetch_l2_4d(&tm_q, nb * 64, (tp % a.n_qt) * BK, (tp / a.n_qt) % a.heads_q,
+                                      (tp / a.n_qt) / a.heads_q);
+          }
+        }
         ptx::mbar_wait(&q_empty[qb], ((it / C::NQB) & 1u) ^ 1u);
         ptx::mbar_arrive_expect_tx(&q_full[qb], C::Q_BYTES);
         const int bh = tile / a.n_qt, qt = tile % a.n_qt;
@@ -590,6 +604,13 @@ static fs_status run(const fs_fwd_params* p, const Plan& pl, uint8_t* ws, cudaSt
     a.n_tiles = static_cast<int>(tiles);
     a.scale = p->scale;
     a.eps = p->eps;
+    {
+      static const int pf_env = [] {
+        const char* e = getenv("FLASHSIGN_GRAM_PF");
+        return e ? atoi(e) : -1;
+      }();
+      a.pf = pf_env >= 0 ? pf_env : kGramPrefetch;
+    }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, num_sms_now())));
     auto go = [&](auto kern) {
       const int sm = ApplyCfg<D, 2>::SMEM;
