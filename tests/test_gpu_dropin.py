@@ -192,3 +192,37 @@ def test_multiplicity_call_large_counts():
     for h in range(2):
         check_rel(got[:, h], gram_spherical(q[:, h].astype(np.float64), kp[:, h], v[:, h].astype(np.float64),
                                             1.0, 1e-6), tag=f"head {h}")
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.float16])
+def test_small_call_path_bitwise_equals_pipeline(monkeypatch, dt):
+    # the packed single-stream path for small calls against the three-stream chunk pipeline
+    from paper_2505_09326_b200 import SPHERICAL, hostpath
+    rng = np.random.default_rng(11)
+    q = rng.standard_normal((77, 4, 40)).astype(dt)
+    k = rng.standard_normal((53, 2, 40)).astype(dt)
+    v = rng.standard_normal((53, 2, 40)).astype(dt)
+    small = att().multi_head_attention_array(q, k, v, SPHERICAL.with_epsilon(1e-6), 4, 2, scale=0.5)
+    monkeypatch.setattr(hostpath, "_SMALL_BYTES", 0)
+    piped = att().multi_head_attention_array(q, k, v, SPHERICAL.with_epsilon(1e-6), 4, 2, scale=0.5)
+    assert small.dtype == piped.dtype == dt and small.shape == (77, 4, 40)
+    assert np.array_equal(small, piped)
+
+
+def test_small_call_path_bad_row_and_reuse():
+    from paper_2505_09326_b200 import SPHERICAL, DegenerateDenominatorError
+    rng = np.random.default_rng(12)
+    q = rng.standard_normal((30, 2, 8)).astype(np.float32)
+    k = rng.standard_normal((20, 2, 8)).astype(np.float32)
+    v = rng.standard_normal((20, 2, 8)).astype(np.float32)
+    q[7, 1] = 0
+    q[9, 0] = 0
+    with pytest.raises(DegenerateDenominatorError, match="row 9"):
+        att().multi_head_attention_array(q, k, v, SPHERICAL, 2, 2)
+    # the reused packed buffers: a larger then a smaller call, each against the float64 oracle
+    for n, x in ((300, 500), (5, 3)):
+        q = rng.standard_normal((n, 1, 16)).astype(np.float32)
+        k = rng.standard_normal((x, 1, 16)).astype(np.float32)
+        v = rng.standard_normal((x, 1, 16)).astype(np.float32)
+        got = att().multi_head_attention_array(q, k, v, SPHERICAL, 1, 1)
+        check_rel(got[:, 0], gram_spherical(*(a[:, 0].astype(np.float64) for a in (q, k, v))), tag=f"n{n}")
