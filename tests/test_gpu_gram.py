@@ -143,3 +143,32 @@ def test_gram_rejects_what_it_cannot_do():
     kv2 = rand_bshd(1, 16, 2, 64, torch.bfloat16, 22)
     with pytest.raises(ConfigError):
         fs().gram_fwd(rand_bshd(1, 16, 3, 64, torch.bfloat16, 21), kv2, kv2)
+
+
+def _gram_cases():
+    # FS_GRAM_N / FS_SWEEP_SEED widen it for stress runs (default 16 cases)
+    import os
+    rng = np.random.default_rng(int(os.environ.get("FS_SWEEP_SEED", 41)))
+    out = []
+    for i in range(int(os.environ.get("FS_GRAM_N", 16))):
+        hkv = int(rng.choice([1, 2, 3]))
+        out.append(dict(dt=[torch.bfloat16, torch.float16][i % 2], b=int(rng.integers(1, 4)),
+                        nq=int(rng.integers(1, 1200)), nkv=int(rng.integers(64, 5000)), h=hkv * int(rng.choice([1, 2, 4])),
+                        hkv=hkv, d=int(rng.choice([8, 16, 24, 32, 40, 48, 56, 64, 72, 96, 112, 128])),
+                        scale=float(rng.choice([1.0, -0.5, 2.0])), eps=float(rng.choice([0.0, 1e-6, 1e-2])),
+                        seed=int(rng.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("c", _gram_cases(), ids=lambda c: f"{str(c['dt'])[6:]}-b{c['b']}-n{c['nq']}x{c['nkv']}-"
+                                                            f"h{c['h']}/{c['hkv']}-d{c['d']}")
+def test_gram_random_sweep(c):
+    q = rand_bshd(c["b"], c["nq"], c["h"], c["d"], c["dt"], c["seed"])
+    k = rand_bshd(c["b"], c["nkv"], c["hkv"], c["d"], c["dt"], c["seed"] + 1)
+    v = rand_bshd(c["b"], c["nkv"], c["hkv"], c["d"], c["dt"], c["seed"] + 2)
+    ref = oracle_of(q, k, v, c["scale"], c["eps"])
+    o = fs().gram_fwd(q, k, v, scale=c["scale"], eps=c["eps"], out_dtype=torch.float32)
+    assert rel_fro(o.cpu().numpy(), ref) <= 2e-4, c
+    # the same contract as the FlashSign kernel, to its (P-rounding) tolerance
+    f = fs().fwd(q, k, v, scale=c["scale"], eps=c["eps"], out_dtype=torch.float32)
+    assert rel_fro(f.cpu().numpy(), ref) <= (4e-3 if c["dt"] == torch.float16 else 1.5e-2), c
