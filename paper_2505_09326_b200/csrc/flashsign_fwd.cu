@@ -71,6 +71,7 @@ namespace fs {
 
 #if FS_PROF
 __device__ unsigned long long g_prof[16];
+__device__ unsigned long long g_cta_t[1024][6];  // per CTA: entry, set-up done, work done, exit (globaltimer), smid, work tiles
 #define FS_PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
 #else
 #define FS_PROF_ADD(i, v)
@@ -493,6 +494,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // clusters of CL CTAs walk the work tiles together (same K/V stream, adjacent query blocks)
   const int rank = CL > 1 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
   const int tile0 = static_cast<int>(blockIdx.x) / CL, tstride = static_cast<int>(gridDim.x) / CL;
+#if FS_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[blockIdx.x][0] = ptx::globaltimer();
+#endif
 
   if (threadIdx.x == 32) {
 #pragma unroll
@@ -540,6 +544,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+#if FS_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[blockIdx.x][1] = ptx::globaltimer();
+#endif
   // CTA pair: the leader (rank 0) owns the barriers the MMAs wait on (q_full, kv_full, p_full,
   // o_empty); the peer's TMA loads complete on them and its norm / epilogue warps arrive remotely
   auto lead = [&](uint64_t* bar) { return ptx::mapa(ptx::smem_u32(bar), 0u); };
@@ -1285,6 +1292,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   // peer mode: the partials went to other GPUs' memory; make them visible system-wide before exit
   if (PEER && warp >= WARP_EPI) __threadfence_system();
+#if FS_PROF
+  if (warp == WARP_EPI && lane == 0 && blockIdx.x < 1024) {
+    g_cta_t[blockIdx.x][2] = ptx::globaltimer();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_cta_t[blockIdx.x][4] = smid;
+    g_cta_t[blockIdx.x][5] = tile0 < p.n_tiles ? (p.n_tiles - 1 - tile0) / tstride + 1 : 0;
+  }
+#endif
   ptx::tc_fence_before();
   if constexpr (C::P2) {
     ptx::cluster_sync();  // both CTAs are done with the pair's TMEM and with each other's barriers
@@ -1300,6 +1316,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   if (CL > 1) ptx::cluster_sync();  // no CTA leaves while its peer may still signal it
+#if FS_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[blockIdx.x][3] = ptx::globaltimer();
+#endif
 }
 
 // ====================================================================== host
@@ -1985,6 +2004,11 @@ int fs_prof_read(unsigned long long* out8) {
   if (cudaMemcpyFromSymbol(out8, fs::g_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
   unsigned long long z[16] = {0};
   return cudaMemcpyToSymbol(fs::g_prof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+// per-CTA timeline of the last launch: [1024][6] (entry, set-up done, work done, exit: globaltimer
+// ns; SM id; work tiles)
+int fs_prof_timeline(unsigned long long* out6144) {
+  return cudaMemcpyFromSymbol(out6144, fs::g_cta_t, sizeof(unsigned long long) * 6144) == cudaSuccess ? 0 : 1;
 }
 #endif
 

@@ -62,12 +62,15 @@ def run(cases, rounds):
         lib.fs_fwd.argtypes = [ctypes.POINTER(_lib.FsFwdParams), ctypes.c_void_p]
         lib.fs_fwd.restype = ctypes.c_int
         lib.fs_last_error.restype = ctypes.c_char_p
+        if hasattr(lib, "fs_prof_timeline"):
+            lib.fs_prof_timeline.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
         libs[os.path.basename(path)[6:-3]] = lib
     tdt = {"fp16": torch.float16, "bf16": torch.bfloat16, "e4m3": torch.float8_e4m3fn}
     code = {"fp16": _lib.FS_F16, "bf16": _lib.FS_BF16, "e4m3": _lib.FS_E4M3}
     res = {}
     for cname in cases:
-        B, N, H, D, dt, eps = CASES[cname]
+        auto = cname.endswith("a")
+        B, N, H, D, dt, eps = CASES[cname[:-1] if auto else cname]
         g = torch.Generator(device="cuda").manual_seed(0)
         q, k, v = (torch.randn((B, N, H, D), generator=g, device="cuda").to(tdt[dt]) for _ in range(3))
         odt = torch.float16 if dt == "fp16" else torch.bfloat16
@@ -81,6 +84,13 @@ def run(cases, rounds):
         p.in_dtype, p.out_dtype = code[dt], (_lib.FS_F16 if dt == "fp16" else _lib.FS_BF16)
         p.scale, p.eps, p.p_scale, p.q_descale, p.k_descale, p.v_descale = 1.0, eps, 1.0, 1.0, 1.0, 1.0
         p.bad_key = bad.data_ptr()
+        if auto:  # the library's split plan (tail-wave K/V split + merge), as flashsign.fwd runs it
+            lib0 = next(iter(libs.values()))
+            lib0.fs_partial_floats.restype = ctypes.c_int64
+            p.kv_splits = _lib.FS_SPLITS_AUTO
+            nf = lib0.fs_partial_floats(ctypes.byref(p))
+            part = torch.empty(max(1, nf), dtype=torch.float32, device="cuda")
+            p.partial = part.data_ptr()
         if cname.endswith("m"):
             m = torch.randint(0, 6, (B, N), generator=g, device="cuda").float()
             p.key_scale, p.key_scale_stride = m.data_ptr(), m.stride(0)
@@ -131,8 +141,27 @@ def run(cases, rounds):
             prof = {"norm_cyc_per_tile": b[0] / max(b[1], 1), "norm_wait_s_cyc": b[6] / max(b[1], 1),
                     "mma_wait_p_cyc": b[2] / max(b[3], 1), "mma_wait_kv_cyc": b[4] / max(b[5], 1),
                     "mma_cyc_per_kv_tile": b[7] / max(b[5], 1)}
+            if hasattr(lib, "fs_prof_timeline"):  # per-CTA globaltimer: entry, set-up, work done, exit
+                tl = (ctypes.c_ulonglong * 6144)()
+                lib.fs_prof_timeline(tl)
+                rows = [tl[6 * i:6 * i + 6] for i in range(1024)]
+                rows = [r for r in rows if r[0] != 0 and r[3] >= r[0]][:148]
+                t0 = min(r[0] for r in rows)
+                t_end = max(r[3] for r in rows)
+                span = t_end - t0
+                q = lambda xs, f: sorted(xs)[min(len(xs) - 1, int(f * len(xs)))]  # noqa: E731
+                starts = [r[0] - t0 for r in rows]
+                dones = [r[2] - t0 for r in rows]
+                prof.update({"ctas": len(rows), "span_us": span / 1e3,
+                             "start_us_p50_max": [q(starts, 0.5) / 1e3, max(starts) / 1e3],
+                             "setup_us_p50": q([r[1] - r[0] for r in rows], 0.5) / 1e3,
+                             "work_done_us_min_p50_max": [min(dones) / 1e3, q(dones, 0.5) / 1e3, max(dones) / 1e3],
+                             "exit_after_done_us_p50": q([r[3] - r[2] for r in rows], 0.5) / 1e3,
+                             "idle_frac": 1.0 - sum(r[3] - r[0] for r in rows) / (len(rows) * span),
+                             "per_cta": [[int(r[4]), int(r[5]), round((r[2] - t0) / 1e3, 2)] for r in rows]})
             res[f"{cname}/{name}/prof"] = prof
-            print(cname, name, "prof", {k: round(v, 1) for k, v in prof.items()}, flush=True)
+            print(cname, name, "prof", {k: (round(v, 3) if isinstance(v, float) else v) for k, v in prof.items()
+                                        if k != "per_cta"}, flush=True)
         ref = next(iter(outs.values()))
         for name in libs:
             tf = statistics.median(x[0] for x in samples[name])
