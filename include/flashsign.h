@@ -32,6 +32,7 @@
 #ifndef FLASHSIGN_H
 #define FLASHSIGN_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -262,6 +263,13 @@ typedef struct {
 } fs_exact_params;
 
 fs_status fs_exact_fwd(const fs_exact_params *p, fs_stream_t stream);
+
+/* ------------------------------------------------------------------ host staging copy
+   Host memory to host memory with non-temporal stores: the drop-in path's fill of its pinned
+   staging slots from the caller's pageable numpy arrays (hostpath.py; the reference's callers
+   pass numpy arrays, attention.py:252-279, 318-361).  No device work.  Returns the vector width
+   used (512, 256) or 0 (plain memcpy). */
+int fs_host_copy(void *dst, const void *src, size_t bytes);
 
 /* Thread-local text of the last non-FS_OK status. */
 const char *fs_last_error(void);

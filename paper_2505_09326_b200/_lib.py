@@ -24,7 +24,7 @@ FS_BAD_NONE = 0xFFFFFFFFFFFFFFFF
 EXPORTED_SYMBOLS = ("fs_fwd", "fs_last_error", "fs_query_tile", "fs_version", "fs_kv_splits", "fs_partial_floats",
                     "fs_combine", "fs_peer_floats", "fs_fwd_peer", "fs_combine_peer", "fs_ipc_malloc", "fs_ipc_open",
                     "fs_ipc_close", "fs_ipc_free", "fs_prepare", "fs_plan", "fs_scale_keys",
-                    "fs_gram_workspace_bytes", "fs_gram_fwd", "fs_exact_fwd")
+                    "fs_gram_workspace_bytes", "fs_gram_fwd", "fs_exact_fwd", "fs_host_copy")
 FS_SPLITS_AUTO = -1
 
 

@@ -18,8 +18,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 OUT = os.path.join(OUT_DIR, "libflashsign.so")
-SOURCES = ["flashsign_fwd.cu", "flashsign_prep.cu", "flashsign_gram.cu", "flashsign_exact.cu"]
-DEPS = ["flashsign_fwd.cu", "flashsign_prep.cu", "flashsign_gram.cu", "flashsign_exact.cu", "sm100.cuh", os.path.join("..", "..", "include", "flashsign.h")]
+SOURCES = ["flashsign_fwd.cu", "flashsign_prep.cu", "flashsign_gram.cu", "flashsign_exact.cu", "fs_host.cpp"]
+DEPS = ["flashsign_fwd.cu", "flashsign_prep.cu", "flashsign_gram.cu", "flashsign_exact.cu", "fs_host.cpp", "sm100.cuh", os.path.join("..", "..", "include", "flashsign.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

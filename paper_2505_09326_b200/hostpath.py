@@ -7,9 +7,9 @@ result dtype back.  Per call, on three CUDA streams of the current device:
 
   copy-in   K and V, then Q in row chunks, cross the host link in the caller's own dtype
             (no host-side conversion pass); arrays of >= 8 MB go through a pinned ring that host
-            threads fill while the DMA engine drains the previous slot (pinned DMA runs ~5x the
-            pageable rate; C3 through the reference's call pattern 54 -> ~115 TFLOP/s, bound
-            by the host-side copy at ~20 GB/s), smaller ones
+            threads fill with non-temporal stores (``fs_host_copy``) while the DMA engine drains
+            the previous slot (pinned DMA runs ~5x the pageable rate; staged copy-in 36-38 GB/s
+            against 11 GB/s pageable and 20-25 GB/s with a numpy fill), smaller ones
             are copied from pageable memory directly (``FLASHSIGN_H2D=auto``, default;
             ``pageable`` / ``staged`` force one)
   compute   ``fs_prepare`` converts each tensor on the device to the kernel's operand
@@ -64,6 +64,15 @@ class _Engine:
         self.pool = None
         self.ring = []
         self.small_host = self.small_dev = None  # packed Q|K|V of small calls (grown on demand)
+        self.copy = None  # staging fill: fs_host_copy (FLASHSIGN_STAGE_COPY=numpy: np.copyto)
+        if os.environ.get("FLASHSIGN_STAGE_COPY", "nt") != "numpy":
+            import ctypes
+
+            from . import _lib
+            fn = _lib.load().fs_host_copy
+            fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+            fn.restype = ctypes.c_int
+            self.copy = fn
         self.small_bad = torch.empty(1, dtype=torch.int64, pin_memory=True)
 
     # ------------------------------------------------------------------ host -> device
@@ -84,14 +93,20 @@ class _Engine:
             self.ring = [(torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
                          for _ in range(3)]
         nthr = self.pool._max_workers
+        src_ptr = flat_src.ctypes.data
         for i, lo in enumerate(range(0, flat_src.size, _STAGE_BYTES)):
             hi = min(lo + _STAGE_BYTES, flat_src.size)
             buf, ev = self.ring[i % len(self.ring)]
             ev.synchronize()  # the DMA that last read this slot is done
-            host = buf.numpy()[:hi - lo]
             step = -(-(hi - lo) // nthr)
-            list(self.pool.map(lambda j: np.copyto(host[j:j + step], flat_src[lo + j:lo + min(j + step, hi - lo)]),
-                               range(0, hi - lo, step)))
+            if self.copy is not None:  # non-temporal stores (csrc/fs_host.cpp; ctypes drops the GIL)
+                dst_ptr = buf.data_ptr()
+                list(self.pool.map(lambda j: self.copy(dst_ptr + j, src_ptr + lo + j, min(step, hi - lo - j)),
+                                   range(0, hi - lo, step)))
+            else:
+                host = buf.numpy()[:hi - lo]
+                list(self.pool.map(lambda j: np.copyto(host[j:j + step], flat_src[lo + j:lo + min(j + step, hi - lo)]),
+                                   range(0, hi - lo, step)))
             with torch.cuda.stream(self.s_h2d):
                 flat_dst[lo:hi].copy_(buf[:hi - lo], non_blocking=True)
                 ev.record(self.s_h2d)

@@ -50,7 +50,11 @@ def one():
     step = -(-slot // nthr)
 
     def fill():
-        list(e.pool.map(lambda j: np.copyto(host[j:j + step], flat[j:j + step]), range(0, slot, step)))
+        if e.copy is not None:
+            dp, sp = e.ring[0][0].data_ptr(), flat.ctypes.data
+            list(e.pool.map(lambda j: e.copy(dp + j, sp + j, min(step, slot - j)), range(0, slot, step)))
+        else:
+            list(e.pool.map(lambda j: np.copyto(host[j:j + step], flat[j:j + step]), range(0, slot, step)))
     t_fill = _best(fill)
     # staged H2D pipeline alone
     dst = torch.empty((n * h, d), dtype=torch.float32, device=dev)
@@ -63,16 +67,19 @@ def one():
     def call():
         multi_head_attention_array(q, k, v, SPHERICAL, h, h, scale=1.0)
     t_call = _best(call)
-    print(json.dumps({"threads": nthr, "slot_mb": slot >> 20, "fill_gbs": slot / t_fill / 1e9,
+    print(json.dumps({"copy": "nt" if e.copy is not None else "numpy", "threads": nthr, "slot_mb": slot >> 20, "fill_gbs": slot / t_fill / 1e9,
                       "staged_h2d_gbs": q.nbytes / t_h2d / 1e9, "call_ms": t_call * 1e3,
                       "call_in_gbs": 3 * q.nbytes / t_call / 1e9, "cpus": os.cpu_count()}), flush=True)
 
 
 def main():
-    for thr in (4, 8, 12, 16):
-        for slot in (16, 32, 64):
-            env = dict(os.environ, FLASHSIGN_H2D_THREADS=str(thr), FLASHSIGN_STAGE_MB=str(slot))
-            subprocess.run([sys.executable, __file__, "--one"], env=env, check=False, timeout=300)
+    for rep in range(2):
+        for copy in ("numpy", "nt"):
+            for thr in (4, 8, 16):
+                for slot in (16, 64):
+                    env = dict(os.environ, FLASHSIGN_H2D_THREADS=str(thr), FLASHSIGN_STAGE_MB=str(slot),
+                               FLASHSIGN_STAGE_COPY=copy)
+                    subprocess.run([sys.executable, __file__, "--one"], env=env, check=False, timeout=300)
 
 
 

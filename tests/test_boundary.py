@@ -332,3 +332,20 @@ def test_integration_c_snippet_compiles(tmp_path):
                     " int N, fs_stream_t stream) {\n" + "\n".join(lines) + "\n}\n")
     subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-c", str(prog), "-o", str(tmp_path / "snippet.o")],
                    check=True)
+
+
+@pytest.mark.parametrize("n", [0, 1, 63, 64, 65, 255, 256, 4097, 1 << 20, (1 << 20) + 37])
+@pytest.mark.parametrize("dst_off,src_off", [(0, 0), (1, 0), (0, 3), (17, 41)])
+def test_host_copy_bitwise(n, dst_off, src_off):
+    # the drop-in staging fill (fs_host_copy, non-temporal stores): host only, any size / alignment
+    import ctypes
+    lib = _lib.load()
+    lib.fs_host_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+    lib.fs_host_copy.restype = ctypes.c_int
+    rng = np.random.default_rng(n + dst_off)
+    src = rng.integers(0, 256, n + src_off + 64, dtype=np.uint8)
+    dst = np.zeros(n + dst_off + 64, dtype=np.uint8)
+    width = lib.fs_host_copy(dst[dst_off:].ctypes.data, src[src_off:].ctypes.data, n)
+    assert width in (0, 256, 512)
+    assert np.array_equal(dst[dst_off:dst_off + n], src[src_off:src_off + n])
+    assert not dst[:dst_off].any() and not dst[dst_off + n:].any()  # nothing outside the range
