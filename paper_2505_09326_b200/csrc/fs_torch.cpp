@@ -192,9 +192,137 @@ py::tuple fwd(const at::Tensor& q, const at::Tensor& k, const at::Tensor& v, c10
   }
 }
 
+int src_code(at::ScalarType t) {
+  switch (t) {
+    case at::kHalf: return FS_F16;
+    case at::kFloat: return FS_F32;
+    case at::kDouble: return FS_F64;
+    default: return -1;
+  }
+}
+
+// The numpy drop-in's small-call path (hostpath._run_small: multi_head_attention_array,
+// attention.py:318-361, on a few MB of host arrays) in one call, so that per-call host time is
+// the copies and launches, not Python: Q|K|V (the caller's C-contiguous numpy buffers, [n, h, d] /
+// [x, h_kv, d], one dtype, passed as addresses) packed into the pinned `host_in`, one H2D copy into `dev_in`,
+// fs_prepare of all three (device-chosen scales into `scales`), fs_fwd with dev_scales (automatic
+// split, as flashsign.fwd_async), the result converted to `host_out_t` on the device and read back
+// into a fresh pinned tensor with the bad-row key, one stream synchronisation.
+// Returns (status, message, host_out [n, h, d_pad], bad_key).
+py::tuple small_call(int64_t q_ptr, int64_t k_ptr, int64_t v_ptr, at::ScalarType src_t, int64_t n, int64_t h,
+                     int64_t x, int64_t hkv, int64_t d, const at::Tensor& host_in, const at::Tensor& dev_in,
+                     const at::Tensor& stats, const at::Tensor& scales, const at::Tensor& bad_host,
+                     at::ScalarType compute, int64_t d_pad, at::ScalarType kout, at::ScalarType host_out_t,
+                     double scale, double eps, int64_t normalizer, bool exact) {
+  try {
+    const int sc = src_code(src_t);
+    const int cc = in_code(compute);
+    const int oc = out_code(kout);
+    if (sc < 0 || cc < 0 || oc < 0) throw Fail{FS_ERR_SHAPE, "flashsign: small_call dtypes"};
+    if (n < 1 || h < 1 || x < 1 || hkv < 1 || d < 1 || d_pad < d || !q_ptr || !k_ptr || !v_ptr)
+      throw Fail{FS_ERR_SHAPE, "flashsign: small_call shapes"};
+    const int64_t isz = c10::elementSize(src_t);
+    auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+    const int64_t nb[3] = {n * h * d * isz, x * hkv * d * isz, x * hkv * d * isz};
+    const int64_t off[3] = {0, al(nb[0]), al(nb[0]) + al(nb[1])};
+    const int64_t tot = off[2] + nb[2];
+    if (!host_in.is_pinned() || host_in.numel() < tot || !dev_in.is_cuda() || dev_in.numel() < tot)
+      throw Fail{FS_ERR_SHAPE, "flashsign: small_call staging buffers too small"};
+    const c10::cuda::CUDAGuard guard(dev_in.device());
+    const auto dopt = dev_in.options();
+    auto stream = at::cuda::getCurrentCUDAStream(dev_in.device().index());
+    const auto cst = stream.stream();
+    auto* hb = static_cast<uint8_t*>(host_in.data_ptr());
+    const int64_t src[3] = {q_ptr, k_ptr, v_ptr};  // the caller's C-contiguous numpy buffers
+    for (int i = 0; i < 3; ++i) std::memcpy(hb + off[i], reinterpret_cast<const void*>(src[i]), nb[i]);
+    auto* db = static_cast<uint8_t*>(dev_in.data_ptr());
+    cudaError_t ce = cudaMemcpyAsync(db, hb, tot, cudaMemcpyHostToDevice, cst);
+    if (ce != cudaSuccess) throw Fail{FS_ERR_CUDA, cudaGetErrorString(ce)};
+
+    at::Tensor qq = at::empty({1, n, h, d_pad}, dopt.dtype(compute));
+    at::Tensor kq = at::empty({1, x, hkv, d_pad}, dopt.dtype(compute));
+    at::Tensor vq = at::empty({1, x, hkv, d_pad}, dopt.dtype(compute));
+    fs_prep_params pp;
+    std::memset(&pp, 0, sizeof(pp));
+    const at::Tensor* dst[3] = {&qq, &kq, &vq};
+    const int64_t rows[3] = {n * h, x * hkv, x * hkv};
+    for (int i = 0; i < 3; ++i) {
+      pp.t[i].src = db + off[i];
+      pp.t[i].src_dtype = sc;
+      pp.t[i].d = static_cast<int32_t>(d);
+      pp.t[i].rows = rows[i];
+      pp.t[i].src_row_stride = d;
+      pp.t[i].dst = dst[i]->data_ptr();
+      pp.t[i].dst_row_stride = d_pad;
+    }
+    pp.dst_dtype = cc;
+    pp.d_pad = static_cast<int32_t>(d_pad);
+    pp.mode = exact ? FS_PREP_EXACT : FS_PREP_SCALE;
+    pp.normalizer = static_cast<int32_t>(normalizer);
+    pp.scale = static_cast<float>(scale);
+    pp.eps = static_cast<float>(eps);
+    pp.stats = stats.data_ptr<double>();
+    pp.scales = scales.data_ptr<float>();
+    fs_status st = fs_prepare(&pp, reinterpret_cast<fs_stream_t>(cst));
+    if (st != FS_OK) throw Fail{static_cast<int>(st), std::string(fs_last_error())};
+
+    at::Tensor o = at::empty({1, n, h, d_pad}, dopt.dtype(kout));
+    at::Tensor bad = at::empty({1}, dopt.dtype(at::kLong));
+    fs_fwd_params p;
+    std::memset(&p, 0, sizeof(p));
+    p.q = qq.data_ptr();
+    p.k = kq.data_ptr();
+    p.v = vq.data_ptr();
+    p.o = o.data_ptr();
+    for (int i = 0; i < 3; ++i) {
+      p.q_stride[i] = qq.stride(i);
+      p.k_stride[i] = kq.stride(i);
+      p.v_stride[i] = vq.stride(i);
+      p.o_stride[i] = o.stride(i);
+    }
+    p.batch = 1;
+    p.heads_q = static_cast<int32_t>(h);
+    p.heads_kv = static_cast<int32_t>(hkv);
+    p.seqlen_q = static_cast<int32_t>(n);
+    p.seqlen_kv = static_cast<int32_t>(x);
+    p.head_dim = static_cast<int32_t>(d_pad);
+    p.in_dtype = static_cast<fs_dtype>(cc);
+    p.out_dtype = static_cast<fs_dtype>(oc);
+    p.scale = static_cast<float>(scale);
+    p.eps = static_cast<float>(eps);
+    p.p_scale = p.q_descale = p.k_descale = p.v_descale = 1.f;
+    p.bad_key = reinterpret_cast<uint64_t*>(bad.data_ptr());
+    p.normalizer = static_cast<int32_t>(normalizer);
+    p.kv_splits = FS_SPLITS_AUTO;
+    p.dev_scales = scales.data_ptr<float>();
+    at::Tensor part;
+    if (fs_kv_splits(&p) > 1) {
+      part = at::empty({fs_partial_floats(&p)}, dopt.dtype(at::kFloat));
+      p.partial = part.data_ptr<float>();
+    }
+    st = fs_fwd(&p, reinterpret_cast<fs_stream_t>(cst));
+    if (st != FS_OK) throw Fail{static_cast<int>(st), std::string(fs_last_error())};
+    at::Tensor res = o[0];
+    if (host_out_t != kout) res = res.to(host_out_t);
+    at::Tensor host_out = at::empty({n, h, d_pad}, at::TensorOptions().dtype(host_out_t).pinned_memory(true));
+    ce = cudaMemcpyAsync(host_out.data_ptr(), res.data_ptr(), host_out.nbytes(), cudaMemcpyDeviceToHost, cst);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(bad_host.data_ptr(), bad.data_ptr(), 8, cudaMemcpyDeviceToHost, cst);
+    if (ce != cudaSuccess) throw Fail{FS_ERR_CUDA, cudaGetErrorString(ce)};
+    {
+      py::gil_scoped_release nogil;
+      ce = cudaStreamSynchronize(cst);
+    }
+    if (ce != cudaSuccess) throw Fail{FS_ERR_CUDA, cudaGetErrorString(ce)};
+    return py::make_tuple(0, std::string(), host_out, *static_cast<int64_t*>(bad_host.data_ptr()));
+  } catch (const Fail& f) {
+    return py::make_tuple(f.status, f.msg, py::none(), 0);
+  }
+}
+
 }  // namespace
 
 PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
+  m.def("small_call", &small_call, "the numpy drop-in's small-call path (hostpath._run_small) in one call");
   m.doc() = "FlashSign torch binding over the C-ABI (include/flashsign.h)";
   m.def("fwd", &fwd, "FlashSign forward on BSHD CUDA tensors (current stream)", py::arg("q"), py::arg("k"),
         py::arg("v"), py::arg("out"), py::arg("out_dtype"), py::arg("bad_key"), py::arg("scale"), py::arg("eps"),

@@ -51,6 +51,14 @@ BAD_NONE = _lib.FS_BAD_NONE
 _ext = None  # the torch extension, bound on first use
 
 
+def torch_ext():
+    """The torch extension over the C-ABI (csrc/fs_torch.cpp), loaded on first use."""
+    global _ext
+    if _ext is None:
+        _ext = _lib.load_torch_ext()
+    return _ext
+
+
 def _check_inputs(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
     for name, t in (("q", q), ("k", k), ("v", v)):
         if not t.is_cuda:

@@ -140,7 +140,8 @@ class _Engine:
         tests): Q|K|V packed into one reused pinned buffer on the host, one H2D copy, one
         ``fs_prepare`` for all three tensors, one FlashSign launch, all on the current stream, and
         one synchronisation -- the multi-stream chunk pipeline of ``run`` only pays off once the
-        copies are long enough to overlap.  Returns ``(out, bad_key, k_device_source)``."""
+        copies are long enough to overlap.  The whole sequence is one C++ call (``small_call`` in
+        csrc/fs_torch.cpp).  Returns ``(out, bad_key, k_device_source)``."""
         n, h, d = q3.shape
         x, hkv, _ = k3.shape
         dev = self.dev
@@ -152,29 +153,15 @@ class _Engine:
             cap = max(tot, 1 << 20)
             self.small_host = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
             self.small_dev = torch.empty(cap, dtype=torch.uint8, device=dev)
-        hb = self.small_host.numpy()
-        for a, o in zip(parts, offs):  # the previous call synchronised, so the buffer is free
-            hb[o:o + a.size] = a
-        stream = torch.cuda.current_stream(dev)
-        with torch.cuda.stream(stream):
-            self.small_dev[:tot].copy_(self.small_host[:tot], non_blocking=True)
-            qr, kr, vr = (self.small_dev[o:o + a.size].view(st).view(-1, d) for a, o in zip(parts, offs))
-            qq = torch.empty((1, n, h, d_pad), dtype=compute, device=dev)
-            kq = torch.empty((1, x, hkv, d_pad), dtype=compute, device=dev)
-            vq = torch.empty((1, x, hkv, d_pad), dtype=compute, device=dev)
-            flashsign.prepare([qr, kr, vr], [qq.view(n * h, d_pad), kq.view(x * hkv, d_pad), vq.view(x * hkv, d_pad)],
-                              stats=self.stats, scales=self.scales, scale=scale, eps=eps, normalizer=normalizer,
-                              exact=exact, stream=stream)
-            oc = torch.empty((1, n, h, d_pad), dtype=k_out, device=dev)
-            bad = torch.empty(1, dtype=torch.int64, device=dev)
-            flashsign.fwd_async(qq, kq, vq, scale=float(scale), eps=float(eps), out=oc, normalizer=normalizer,
-                                bad_key=bad, stream=stream, dev_scales=self.scales)
-            src = oc[0] if host_out_t == k_out else oc[0].to(host_out_t)
-            host_out = torch.empty((n, h, d_pad), dtype=host_out_t, pin_memory=True)
-            host_out.copy_(src, non_blocking=True)
-            self.small_bad.copy_(bad, non_blocking=True)
-        stream.synchronize()
-        return host_out.numpy(), int(self.small_bad.item()), kr
+        ext = flashsign.torch_ext()
+        st_, msg, host_out, bad_key = ext.small_call(
+            q3.ctypes.data, k3.ctypes.data, v3.ctypes.data, st, n, h, x, hkv, d, self.small_host, self.small_dev,
+            self.stats, self.scales, self.small_bad, compute, d_pad, k_out, host_out_t, float(scale), float(eps),
+            flashsign.NORMALIZERS[normalizer], bool(exact))
+        if st_ != 0:
+            raise flashsign._STATUS_EXC.get(st_, RuntimeError)(f"flashsign: {msg}")
+        kr = self.small_dev[offs[1]:offs[1] + parts[1].size].view(st).view(-1, d)  # K as copied (bad-row z)
+        return host_out.numpy(), int(bad_key), kr
 
     # ------------------------------------------------------------------ one call
     def run(self, q3: np.ndarray, k3: np.ndarray, v3: np.ndarray, *, scale: float, eps: float, compute: torch.dtype,
@@ -196,6 +183,9 @@ class _Engine:
         chunks = [(lo, min(lo + cq, n)) for lo in range(0, n, cq)]
         nb = min(2, len(chunks))
         if x > 0 and len(chunks) == 1 and q3.nbytes + k3.nbytes + v3.nbytes <= _SMALL_BYTES:
+            # one source dtype in the packed buffer: K / V in Q's, the rounding the pipeline's
+            # device-side copy_ applies to mixed-dtype callers (the reference accepts those)
+            k3, v3 = (a if a.dtype == q3.dtype else a.astype(q3.dtype) for a in (k3, v3))
             out, bad_key, kr = self._run_small(q3, k3, v3, scale=scale, eps=eps, compute=compute,
                                                normalizer=normalizer, exact=exact, d_pad=d_pad, k_out=k_out,
                                                host_out_t=host_out_t, st=st)

@@ -301,3 +301,22 @@ def test_dropin_random_sweep(c):
         tol = 1e-5
     worst = float((np.abs(got.astype(np.float64) - ref) / cond).max())
     assert worst <= tol, (c, worst)
+
+
+@pytest.mark.parametrize("dts", [(np.float32, np.float64, np.float32), (np.float64, np.float32, np.float16),
+                                 (np.float16, np.float32, np.float64)])
+def test_mixed_dtype_arrays_small_and_pipeline(monkeypatch, dts):
+    # the reference accepts q, k, v of different float dtypes (result in q's dtype)
+    from paper_2505_09326_b200 import SPHERICAL, hostpath
+    rng = np.random.default_rng(13)
+    q = rng.standard_normal((40, 2, 16)).astype(dts[0])
+    k = rng.standard_normal((60, 1, 16)).astype(dts[1])
+    v = rng.standard_normal((60, 1, 16)).astype(dts[2])
+    small = att().multi_head_attention_array(q, k, v, SPHERICAL, 2, 1)
+    monkeypatch.setattr(hostpath, "_SMALL_BYTES", 0)
+    piped = att().multi_head_attention_array(q, k, v, SPHERICAL, 2, 1)
+    assert small.dtype == piped.dtype == dts[0]
+    assert np.array_equal(small, piped)
+    ref = np.stack([gram_spherical(q[:, i].astype(np.float64), k[:, 0].astype(np.float64),
+                                   v[:, 0].astype(np.float64)) for i in range(2)], axis=1)
+    check_rel(small, ref, 3e-3, 1.5e-2)
