@@ -234,7 +234,12 @@ py::tuple small_call(int64_t q_ptr, int64_t k_ptr, int64_t v_ptr, at::ScalarType
     const auto cst = stream.stream();
     auto* hb = static_cast<uint8_t*>(host_in.data_ptr());
     const int64_t src[3] = {q_ptr, k_ptr, v_ptr};  // the caller's C-contiguous numpy buffers
-    for (int i = 0; i < 3; ++i) std::memcpy(hb + off[i], reinterpret_cast<const void*>(src[i]), nb[i]);
+    for (int i = 0; i < 3; ++i) {  // streaming stores past a few hundred KB (no read-for-ownership)
+      if (nb[i] >= (256 << 10))
+        fs_host_copy(hb + off[i], reinterpret_cast<const void*>(src[i]), static_cast<size_t>(nb[i]));
+      else
+        std::memcpy(hb + off[i], reinterpret_cast<const void*>(src[i]), nb[i]);
+    }
     auto* db = static_cast<uint8_t*>(dev_in.data_ptr());
     cudaError_t ce = cudaMemcpyAsync(db, hb, tot, cudaMemcpyHostToDevice, cst);
     if (ce != cudaSuccess) throw Fail{FS_ERR_CUDA, cudaGetErrorString(ce)};

@@ -20,7 +20,7 @@ result dtype back.  Per call, on three CUDA streams of the current device:
   copy-out  each chunk's O goes by DMA straight into a pinned host array, which is the
             returned result (no host copy on the way out)
 
-Calls with at most 4 MB of input in one chunk (the GRN per-cell shapes, the reference's own
+Calls with at most 12 MB of input in one chunk (the GRN per-cell shapes, the reference's own
 tests) skip the three-stream pipeline: Q|K|V packed into one pinned buffer, one copy, one
 ``fs_prepare``, one launch and one synchronisation on the current stream (``_run_small``).
 
@@ -43,7 +43,9 @@ _SRC_TORCH = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.f
               np.dtype(np.float16): torch.float16}
 _CHUNK_BYTES = int(os.environ.get("FLASHSIGN_CHUNK_MB", "32")) << 20
 _STAGE_MIN_BYTES = 8 << 20  # auto mode: pinned staging from this size on
-_SMALL_BYTES = 4 << 20  # Q + K + V up to this size: one packed copy, one stream (``_run_small``)
+# Q + K + V up to this size: one packed copy, one stream (``_run_small``); measured faster than the
+# pipeline up to ~4 MB per array (tests/size_sweep.py: 2 MB arrays 639 vs 816 us, 4 MB equal)
+_SMALL_BYTES = 12 << 20
 # pinned ring slot: 64 MB measured best for the host-thread fill (C3 drop-in 95 -> 116 TFLOP/s vs 32 MB)
 _STAGE_BYTES = int(os.environ.get("FLASHSIGN_STAGE_MB", "64")) << 20
 
