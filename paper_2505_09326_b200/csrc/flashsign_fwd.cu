@@ -143,6 +143,12 @@ constexpr int NQT = 2;   // Q tiles per work tile
 #ifndef FS_DEFER_Z
 #define FS_DEFER_Z 1  // 16-bit inputs: the norm warps' last-chunk a2(s) accumulation after the P hand-off
 #endif
+#ifndef FS_NORM_DB
+// 16-bit inputs: the norm warps read S in 16-column chunks into two register buffers, the next
+// chunk's TMEM load in flight while this chunk is converted (instead of 32-column chunks, one buffer)
+#define FS_NORM_DB 0  // measured slower: experiment knob
+#endif
+
 #ifndef FS_P2_STAGES
 #define FS_P2_STAGES 0  // CTA-pair ring depth override (0: as many half-tile slots as fit)
 #endif
@@ -1003,12 +1009,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         // BN/2 columns in 32-column chunks (80 registers/thread at 768 threads): the next chunk's
         // TMEM load is issued once this chunk is packed, and overlaps this chunk's P store.
-        constexpr int NCH = BN / 64;
-        // 16-bit P, 192-key tiles: accumulate the last chunk's a2(s) after the P hand-off (FP8: the e4m3 conversion
+        // FS_NORM_DB (16-bit): 16-column chunks, two buffers, the next load issued before this
+        // chunk's conversion so that it overlaps the ALU work.
+        // (Two 32-column buffers do not fit: with setmaxnreg moving the producer / MMA warpgroup to
+        // 24-32 and the epilogue to 40-64 registers, the norm warps get at most 96 and ptxas needs
+        // more -- 768 threads share 80 x 768 registers.)
+        constexpr bool DB = FS_NORM_DB && !TR::F8;
+        constexpr int CW = DB ? 16 : 32;  // columns per chunk
+        constexpr int NCH = (BN / 2) / CW;
+        // 16-bit P, 192-key tiles: accumulate the last 32 columns' a2(s) after the P hand-off (FP8: the e4m3 conversion
         // runs on its own pipe and hides the FFMA2s; its saturation check needs the sums first)
-        constexpr bool DEFER_Z = FS_DEFER_Z && !TR::F8 && NCH >= 3 && !C::ZP;
-        uint32_t s[32];
-        ptx::tmem_ld32(s_addr, s);
+        constexpr bool DEFER_Z = FS_DEFER_Z && !TR::F8 && BN / 2 >= 96 && !C::ZP;
+        constexpr int NDEF = DEFER_Z ? 32 / CW : 0;  // deferred chunks (the last ones, still in registers)
+        uint32_t sbuf[DB ? 2 : 1][CW];
+        auto ld_chunk = [&](uint32_t addr, uint32_t* dst) {
+          if constexpr (CW == 16)
+            ptx::tmem_ld16(addr, dst);
+          else
+            ptx::tmem_ld32(addr, dst);
+        };
+        ld_chunk(s_addr, sbuf[0]);
         ptx::tmem_wait_ld();
         // FP8: every chunk's packed codes and the half's sum of a2(s), for one saturation check per
         // half after its last store (off the chunk-to-chunk path)
@@ -1027,12 +1047,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         };
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
+          uint32_t* s = sbuf[DB ? (ch & 1) : 0];
+          if constexpr (DB) {
+            if (ch + 1 < NCH) ld_chunk(s_addr + CW * (ch + 1), sbuf[(ch + 1) & 1]);  // the other buffer
+          }
           // (a2(s) accumulates into the half's h0 / h1 chains)  With KS the scores are
           // first scaled by the key multiplicities, s_ij <- m_j s_ij (fp32; exact for integer m).
           const float4* mp = reinterpret_cast<const float4*>(smem + C::MS_OFF + v_slot * C::MS_SLOT_BYTES) +
-                             (hh * (BN / 2) + ch * 32) / 4;
+                             (hh * (BN / 2) + ch * CW) / 4;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
+          for (int i = 0; i < CW; i += 4) {
             float2 a = make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1]));
             float2 b = make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
             if constexpr (KS && !C::KSM) {
@@ -1044,10 +1068,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               s[i + 2] = __float_as_uint(b.x);
               s[i + 3] = __float_as_uint(b.y);
             }
-            if (!C::ZP && !(DEFER_Z && ch == NCH - 1)) accum_a2(a, b);
+            if (!C::ZP && !(DEFER_Z && ch >= NCH - NDEF)) accum_a2(a, b);
           }
           // pack P (s[i] is written only after s[2i], s[2i+1] / s[4i..4i+3] are read)
-          uint32_t pk_local[16];
+          uint32_t pk_local[CW / 2];
           uint32_t* pk = TR::SAT_CHECK ? pk8 + (TR::SAT_CHECK ? ch * 8 : 0) : pk_local;
           if constexpr (TR::F8) {
             if (ps == 1.0f) {
@@ -1063,18 +1087,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           } else if (ps == 1.0f) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = pack2<IN>(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
+            for (int i = 0; i < CW / 2; ++i) pk[i] = pack2<IN>(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1]));
           } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
+            for (int i = 0; i < CW / 2; ++i)
               pk[i] = pack2<IN>(ps * __uint_as_float(s[2 * i]), ps * __uint_as_float(s[2 * i + 1]));
           }
-          if (ch + 1 < NCH) ptx::tmem_ld32(s_addr + 32 * (ch + 1), s);  // next chunk (s is consumed)
-          if constexpr (TR::F8)
+          if constexpr (!DB) {
+            if (ch + 1 < NCH) ptx::tmem_ld32(s_addr + 32 * (ch + 1), s);  // next chunk (s is consumed)
+          }
+          if constexpr (TR::F8 || CW == 16)
             ptx::tmem_st8(s_addr + ch * 8, pk);
           else
             ptx::tmem_st16(s_addr + ch * 16, pk);
-          if (ch + 1 < NCH) ptx::tmem_wait_ld();
+          if (ch + 1 < NCH) {
+            if constexpr (CW == 16)
+              ptx::tmem_wait_ld16(sbuf[(ch + 1) & 1]);
+            else
+              ptx::tmem_wait_ld();
+          }
         }
         if constexpr (!DEFER_Z && !C::ZP) {
           za = __fadd2_rn(za, h0);
@@ -1131,12 +1162,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           za.y += (zc[2] + zc[3]) * inv_pz;
         }
         if constexpr (DEFER_Z) {
-          // the last chunk's a2(s) after P is handed over: off the P critical path (16-bit P: the
-          // FFMA2s share the conversion's pipe); s still holds that chunk
+          // the last 32 columns' a2(s) after P is handed over: off the P critical path (16-bit P:
+          // the FFMA2s share the conversion's pipe); the buffers still hold those chunks
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            accum_a2(make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1])),
-                     make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
+          for (int c = NCH - NDEF; c < NCH; ++c) {
+            const uint32_t* s = sbuf[DB ? (c & 1) : 0];
+#pragma unroll
+            for (int i = 0; i < CW; i += 4)
+              accum_a2(make_float2(__uint_as_float(s[i + 0]), __uint_as_float(s[i + 1])),
+                       make_float2(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
+          }
           za = __fadd2_rn(za, h0);
           zb = __fadd2_rn(zb, h1);
         }
