@@ -49,6 +49,9 @@ namespace gram {
 
 constexpr int BK = 128;             // keys per K/V tile (launch 1) = query rows per tile (launch 3)
 constexpr int kGramPrefetch = 0;    // apply kernel: L2 prefetch distance of Q tiles (FLASHSIGN_GRAM_PF)
+#ifndef FS_GRAM_NQB128
+#define FS_GRAM_NQB128 2  // apply kernel, d = 128: Q tile buffers (3 fit, measured no faster)
+#endif
 constexpr int BLK = BK * 128;       // one SW128 column block: 128 rows x 64 16-bit elements
 
 template <int D>
@@ -266,11 +269,17 @@ __global__ void __launch_bounds__(128) gram_reduce_kernel(const float* __restric
 template <int D, int NT>
 struct ApplyCfg {
   static constexpr int Q_BYTES = BK * D * 2;
-  static constexpr int NQB = NT == 1 ? 4 : 2;
+  // Q buffers: as many as fit beside the B image (d = 128: 3 x 32 KB + 128 KB, with the barrier
+  // block trimmed to 3 KB and no alignment slack -- the kernel checks the base is 1024-aligned)
+  static constexpr int NQB = NT == 1 ? 4 : (D == 128 ? FS_GRAM_NQB128 : 4);
   static constexpr int IMG_OFF = NQB * Q_BYTES;
   static constexpr int IMG_BYTES = NT * ImgCfg<D>::TERM;
   static constexpr int BAR_OFF = IMG_OFF + IMG_BYTES;
-  static constexpr int SMEM = BAR_OFF + 4096 + 1024;  // barriers + the epilogue's z exchange (2 KB)
+  static constexpr int BAR_BYTES = 3072;  // barriers (128 B) + the epilogue's z exchange (2 KB)
+  static constexpr int SLACK = BAR_OFF + BAR_BYTES + 1024 <= 232448 ? 1024 : 0;
+  static constexpr int SMEM = BAR_OFF + BAR_BYTES + SLACK;
+  static_assert(SMEM <= 232448, "gram apply: shared memory");
+  static_assert(NQB <= 4, "q_full / q_empty hold 4 barriers each");
   static constexpr int TN = 2 * D;  // accumulator columns per buffer
   static constexpr int TCOLS = 2 * TN;
 };
@@ -317,6 +326,7 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
   using C = ApplyCfg<D, NT>;
   constexpr int NB = D / 64;
   extern __shared__ uint8_t smem_raw[];
+  if (C::SLACK == 0 && (ptx::smem_u32(smem_raw) & 1023u) != 0) __trap();  // layout needs an aligned base
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t *q_full = bars, *q_empty = bars + 4, *t_full = bars + 8, *t_empty = bars + 10;
@@ -436,9 +446,8 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
         sG = a.scl[2 * kv + 1];
         cur_kv = kv;
       }
-      // this row's half of q, straight from the swizzled Q tile as soon as it lands, so the Q buffer
-      // frees when the MMAs finish (not after the accumulator is drained): the producer can keep
-      // the next-but-one tile's load in flight
+      // this row's half of q, straight from the swizzled Q tile as soon as it lands (the buffer is
+      // released once the partial z below has consumed it)
       ptx::mbar_wait(&q_full[qb], (it / C::NQB) & 1u);
       const uint8_t* qrow = smem + qb * C::Q_BYTES + r * 128;
       uint4 qv[HD / 8];
@@ -447,8 +456,6 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
         const int chunk = hf * (HD / 8) + j, kb = chunk >> 3, cj = chunk & 7;
         qv[j] = *reinterpret_cast<const uint4*>(qrow + kb * BLK + ((cj ^ (r & 7)) << 4));
       }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&q_empty[qb]);
       ptx::mbar_wait(&t_full[tb], (it >> 1) & 1u);
       ptx::tc_fence_after();
       // partial z = sum over this half's columns a of T^G_a q_a
@@ -478,7 +485,13 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
       ptx::tmem_wait_ld();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&t_empty[tb]);
+      if (lane == 0) {
+        ptx::mbar_arrive(&t_empty[tb]);
+        // Q buffer released only now that q has been consumed (the partial z above): an arrive
+        // right after the shared loads let the next TMA load overwrite the tile before those
+        // loads had returned (bad rows at C3 size, many tiles per CTA; tests/test_gpu_gram.py)
+        ptx::mbar_arrive(&q_empty[qb]);
+      }
       const int row = qt * BK + r;
       const bool live = row < a.seqlen_q;
       // the reference's z and denominator (normalizers.py:83-91); Gram rounding can leave a tiny
