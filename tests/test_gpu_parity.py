@@ -1031,3 +1031,19 @@ def test_long_sequence_million_keys():
     # and split into 4 K/V ranges of 2^18 keys (partials + merge kernel)
     o2 = fs().fwd(q, k, v, kv_splits=4)
     check_tol(o2[0, rows.cuda(), 0].float().cpu().numpy(), ref, torch.bfloat16, "N=2^20 split 4")
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_full_size_repeat_launches_bitwise(name):
+    # a race between the kernel's roles shows up as launch-to-launch differences at full size
+    # (many work tiles per CTA, the tail-split merge, the K' pass for C5's multiplicities)
+    b, n, h, d, dt = {"c3": (8, 16384, 16, 128, torch.bfloat16), "c4": (8, 8192, 16, 128, torch.float8_e4m3fn),
+                      "c5": (64, 20000, 8, 64, torch.bfloat16)}[name]
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q, k, v = (torch.randn((b, n, h, d), generator=g, device="cuda").to(dt) for _ in range(3))
+    m = torch.randint(0, 6, (b, n), generator=g, device="cuda").float() if name == "c5" else None
+    eps = 1e-6 if name == "c5" else 0.0
+    ref = fs().fwd(q, k, v, out_dtype=torch.bfloat16, key_scale=m, eps=eps)
+    for _ in range(6):
+        o = fs().fwd(q, k, v, out_dtype=torch.bfloat16, key_scale=m, eps=eps)
+        assert torch.equal(o.view(torch.int16), ref.view(torch.int16))
