@@ -92,6 +92,7 @@ class ClockSampler:
     def __init__(self, index: int, period_s: float = 0.005):
         self.index, self.period = index, period_s
         self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.power_mw, self.limit_w = [], None
         self._stop = threading.Event()
         self._t = None
         try:
@@ -100,6 +101,10 @@ class ClockSampler:
             self.nvml = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+            except Exception:
+                pass
         except Exception:
             self.nvml = None
 
@@ -107,6 +112,12 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                try:  # instantaneous board power (GetPowerUsage is a ~1 s average, too slow here)
+                    fv = self.nvml.nvmlDeviceGetFieldValues(self.h, [self.nvml.NVML_FI_DEV_POWER_INSTANT])[0]
+                    if fv.nvmlReturn == 0:
+                        self.power_mw.append(fv.value.uiVal)
+                except Exception:
+                    pass
                 r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
@@ -129,8 +140,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power_mw:  # board power during the timed region (clock and power)
+            out["power_w"] = statistics.median(self.power_mw) / 1000.0  # NVML_FI_DEV_POWER_INSTANT
+            out["power_limit_w"] = self.limit_w
+        return out
 
 
 def make_inputs(cfg, lo, hi, device, seed=1000):
