@@ -106,12 +106,18 @@ def run(cases, rounds):
                     rc = lib.fs_fwd(ctypes.byref(p), ctypes.c_void_p(s))
                     assert rc == 0, lib.fs_last_error()
                 torch.cuda.synchronize()
-                clk, stop = [], threading.Event()
+                clk, pw, stop = [], [], threading.Event()
 
                 def sampler():
                     while not stop.is_set():
                         if pynvml is not None:
                             clk.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                            try:
+                                fv = pynvml.nvmlDeviceGetFieldValues(h, [pynvml.NVML_FI_DEV_POWER_INSTANT])[0]
+                                if fv.nvmlReturn == 0:
+                                    pw.append(fv.value.uiVal / 1000.0)
+                            except Exception:
+                                pass
                         time.sleep(0.01)
                 th = threading.Thread(target=sampler, daemon=True)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -125,8 +131,9 @@ def run(cases, rounds):
                 th.join()
                 ms = e0.elapsed_time(e1) / n
                 mhz = statistics.median(clk) if clk else float("nan")
+                watts = statistics.median(pw) if pw else float("nan")
                 if rnd > 0:  # round 0 is a warm-up
-                    samples[name].append((flops / ms / 1e9, mhz))
+                    samples[name].append((flops / ms / 1e9, mhz, watts))
                 if rnd == 1:
                     outs[name] = o.float().clone()
         for name, lib in libs.items():  # diagnostic builds (-DFS_PROF=1): per-event latencies, one launch
@@ -167,7 +174,9 @@ def run(cases, rounds):
             tf = statistics.median(x[0] for x in samples[name])
             mhz = statistics.median(x[1] for x in samples[name])
             diff = float((outs[name] - ref).abs().max())
+            watts = statistics.median(x[2] for x in samples[name])
             res[f"{cname}/{name}"] = {"tflops": round(tf, 1), "sm_mhz": mhz, "tflops_per_ghz": round(tf / mhz * 1e3, 1),
+                                      "power_w": round(watts, 1), "tflops_per_kw": round(tf / watts * 1e3, 1),
                                       "max_abs_vs_first": diff, "launches_per_sample": n}
             print(cname, name, res[f"{cname}/{name}"], flush=True)
         del q, k, v, o
