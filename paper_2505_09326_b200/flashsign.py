@@ -24,7 +24,6 @@ synchronising (benchmarks).
 from __future__ import annotations
 
 import ctypes
-import math
 
 import torch
 
