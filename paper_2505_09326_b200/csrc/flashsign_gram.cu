@@ -49,6 +49,17 @@ namespace gram {
 
 constexpr int BK = 128;             // keys per K/V tile (launch 1) = query rows per tile (launch 3)
 constexpr int kGramPrefetch = 0;    // apply kernel: L2 prefetch distance of Q tiles (FLASHSIGN_GRAM_PF)
+#ifndef FS_GRAM_PROF
+#define FS_GRAM_PROF 0  // diagnostic build: per-role wait counters of the apply kernel (fs_gram_prof_read)
+#endif
+#if FS_GRAM_PROF
+__device__ unsigned long long g_gprof[8];
+#define GPROF_ADD(i, v) atomicAdd(&g_gprof[i], (unsigned long long)(v))
+#define GPROF_T() clock64()
+#else
+#define GPROF_ADD(i, v)
+#define GPROF_T() 0ll
+#endif
 #ifndef FS_GRAM_NQB128
 #define FS_GRAM_NQB128 2  // apply kernel, d = 128: Q tile buffers (3 fit, measured no faster)
 #endif
@@ -386,7 +397,9 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
                                       (tp / a.n_qt) / a.heads_q);
           }
         }
+        const long long tp0 = GPROF_T();
         ptx::mbar_wait(&q_empty[qb], ((it / C::NQB) & 1u) ^ 1u);
+        GPROF_ADD(4, GPROF_T() - tp0);
         ptx::mbar_arrive_expect_tx(&q_full[qb], C::Q_BYTES);
         const int bh = tile / a.n_qt, qt = tile % a.n_qt;
 #pragma unroll
@@ -399,6 +412,7 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
     const uint32_t lp = ptx::elect_one() ? 1u : 0u;
     constexpr uint32_t idesc = ptx::idesc_make(fmt<IN>(), fmt<IN>(), 0, 0, 128, C::TN);
     int cur = -1, n_img = 0;
+    const long long tm0 = GPROF_T();
     for (int tile = tb0, it = 0; tile < tb1; ++tile, ++it) {
       const int kv = bhkv_of(tile);
       if (kv != cur) {
@@ -407,8 +421,15 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
         ++n_img;
       }
       const int qb = it % C::NQB, tb = it & 1;
+      const long long tq0 = GPROF_T();
       ptx::mbar_wait(&q_full[qb], (it / C::NQB) & 1u);
+      const long long tq1 = GPROF_T();
       ptx::mbar_wait(&t_empty[tb], ((it >> 1) & 1u) ^ 1u);
+      if (lp) {
+        GPROF_ADD(0, tq1 - tq0);
+        GPROF_ADD(1, GPROF_T() - tq1);
+        GPROF_ADD(3, 1);
+      }
       ptx::tc_fence_after();
       const uint32_t qa = ptx::smem_u32(smem + qb * C::Q_BYTES);
       const uint32_t ia = ptx::smem_u32(smem + C::IMG_OFF);
@@ -425,6 +446,7 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
       ptx::tc_commit_p(&q_empty[qb], lp);
       if (tile + 1 >= tb1 || bhkv_of(tile + 1) != kv) ptx::tc_commit_p(img_empty, lp);
     }
+    if (lp) GPROF_ADD(2, GPROF_T() - tm0);
   } else {
     // epilogue, 8 warps: warp w reads TMEM lane quarter w % 4 (rows r) and column half hf of both
     // moments -- partial z over its half of G's columns, exchanged with its partner warp (same
@@ -456,7 +478,9 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
         const int chunk = hf * (HD / 8) + j, kb = chunk >> 3, cj = chunk & 7;
         qv[j] = *reinterpret_cast<const uint4*>(qrow + kb * BLK + ((cj ^ (r & 7)) << 4));
       }
+      const long long te0 = GPROF_T();
       ptx::mbar_wait(&t_full[tb], (it >> 1) & 1u);
+      if (warp == 2 && lane == 0) GPROF_ADD(5, GPROF_T() - te0);
       ptx::tc_fence_after();
       // partial z = sum over this half's columns a of T^G_a q_a
       uint32_t t[NL][32];
@@ -646,6 +670,14 @@ static fs_status run(const fs_fwd_params* p, const Plan& pl, uint8_t* ws, cudaSt
 
 }  // namespace gram
 }  // namespace fs
+
+#if FS_GRAM_PROF
+extern "C" int fs_gram_prof_read(unsigned long long* out8) {
+  if (cudaMemcpyFromSymbol(out8, fs::gram::g_gprof, sizeof(unsigned long long) * 8) != cudaSuccess) return 1;
+  unsigned long long z[8] = {0};
+  return cudaMemcpyToSymbol(fs::gram::g_gprof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 extern "C" {
 

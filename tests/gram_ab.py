@@ -57,6 +57,21 @@ def run():
                 if rnd:
                     res.setdefault(name, []).append(e0.elapsed_time(e1) / 30)
                 outs[name] = o.clone()
+        for name, lib in libs.items():  # -DFS_GRAM_PROF=1 builds: per-role waits of the apply kernel
+            if not hasattr(lib, "fs_gram_prof_read"):
+                continue
+            buf = (ctypes.c_ulonglong * 8)()
+            wb = lib.fs_gram_workspace_bytes(ctypes.byref(p))
+            ws = torch.empty(wb, dtype=torch.uint8, device="cuda")
+            lib.fs_gram_prof_read(buf)
+            lib.fs_gram_fwd(ctypes.byref(p), ctypes.c_void_p(ws.data_ptr()), ctypes.c_int64(wb), ctypes.c_void_p(s))
+            torch.cuda.synchronize()
+            lib.fs_gram_prof_read(buf)
+            b = list(buf)
+            nt = max(b[3], 1)
+            print(cname, name, "per tile (cycles): mma wait q_full", b[0] // nt, "mma wait t_empty", b[1] // nt,
+                  "mma loop", b[2] // nt, "producer wait q_empty", b[4] // nt, "epilogue(warp 2) wait t_full",
+                  b[5] // nt, "tiles", b[3], flush=True)
         ref = next(iter(outs.values()))
         for name in libs:
             ms = sorted(res[name])[len(res[name]) // 2]
