@@ -61,7 +61,7 @@ __device__ unsigned long long g_gprof[8];
 #define GPROF_T() 0ll
 #endif
 #ifndef FS_GRAM_NQB128
-#define FS_GRAM_NQB128 2  // apply kernel, d = 128: Q tile buffers (3 fit, measured no faster)
+#define FS_GRAM_NQB128 3  // apply kernel, d = 128: Q tile buffers (227 KB of shared memory)
 #endif
 constexpr int BLK = BK * 128;       // one SW128 column block: 128 rows x 64 16-bit elements
 
@@ -281,7 +281,8 @@ template <int D, int NT>
 struct ApplyCfg {
   static constexpr int Q_BYTES = BK * D * 2;
   // Q buffers: as many as fit beside the B image (d = 128: 3 x 32 KB + 128 KB, with the barrier
-  // block trimmed to 3 KB and no alignment slack -- the kernel checks the base is 1024-aligned)
+  // block trimmed to 3 KB and no alignment slack -- the kernel checks the base is 1024-aligned);
+  // the third buffer pays once the MMA issue loop is no longer the limit (C3 -5 %)
   static constexpr int NQB = NT == 1 ? 4 : (D == 128 ? FS_GRAM_NQB128 : 4);
   static constexpr int IMG_OFF = NQB * Q_BYTES;
   static constexpr int IMG_BYTES = NT * ImgCfg<D>::TERM;
@@ -411,6 +412,8 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
   } else if (warp == 1) {
     const uint32_t lp = ptx::elect_one() ? 1u : 0u;
     constexpr uint32_t idesc = ptx::idesc_make(fmt<IN>(), fmt<IN>(), 0, 0, 128, C::TN);
+    const uint64_t q_desc0 = ptx::sdesc_sw128(ptx::smem_u32(smem), 16, 1024);
+    const uint64_t img_desc0 = ptx::sdesc_sw128(ptx::smem_u32(smem + C::IMG_OFF), 16, 1024);
     int cur = -1, n_img = 0;
     const long long tm0 = GPROF_T();
     for (int tile = tb0, it = 0; tile < tb1; ++tile, ++it) {
@@ -431,16 +434,17 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
         GPROF_ADD(3, 1);
       }
       ptx::tc_fence_after();
-      const uint32_t qa = ptx::smem_u32(smem + qb * C::Q_BYTES);
-      const uint32_t ia = ptx::smem_u32(smem + C::IMG_OFF);
+      // descriptors: one base per operand, per-step offsets are constants (address field in 16 B
+      // units) -- rebuilding both descriptors per MMA held the issue loop at ~1.6x the MMA time
+      const uint64_t a0 = q_desc0 + static_cast<uint32_t>((qb * C::Q_BYTES) >> 4);
 #pragma unroll
       for (int term = 0; term < NT; ++term)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off_a = (ks * 32 / 128) * BLK + (ks * 32) % 128;
-          const uint32_t off_b = term * ImgCfg<D>::TERM + (ks * 32 / 128) * (ImgCfg<D>::ROWS * 128) + (ks * 32) % 128;
-          ptx::mma_f16_ss_p(tmem + tb * C::TN, ptx::sdesc_sw128(qa + off_a, 16, 1024),
-                            ptx::sdesc_sw128(ia + off_b, 16, 1024), idesc, (term > 0 || ks > 0) ? 1u : 0u, lp);
+          const uint32_t off_a = ((ks * 32 / 128) * BLK + (ks * 32) % 128) >> 4;
+          const uint32_t off_b =
+              (term * ImgCfg<D>::TERM + (ks * 32 / 128) * (ImgCfg<D>::ROWS * 128) + (ks * 32) % 128) >> 4;
+          ptx::mma_f16_ss_p(tmem + tb * C::TN, a0 + off_a, img_desc0 + off_b, idesc, (term > 0 || ks > 0) ? 1u : 0u, lp);
         }
       ptx::tc_commit_p(&t_full[tb], lp);
       ptx::tc_commit_p(&q_empty[qb], lp);
