@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
                                       (tp / a.n_qt) / a.heads_q);
           }
         }
-        const long long tp0 = GPROF_T();
+        [[maybe_unused]] const long long tp0 = GPROF_T();
         ptx::mbar_wait(&q_empty[qb], ((it / C::NQB) & 1u) ^ 1u);
         GPROF_ADD(4, GPROF_T() - tp0);
         ptx::mbar_arrive_expect_tx(&q_full[qb], C::Q_BYTES);
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
     const uint64_t q_desc0 = ptx::sdesc_sw128(ptx::smem_u32(smem), 16, 1024);
     const uint64_t img_desc0 = ptx::sdesc_sw128(ptx::smem_u32(smem + C::IMG_OFF), 16, 1024);
     int cur = -1, n_img = 0;
-    const long long tm0 = GPROF_T();
+    [[maybe_unused]] const long long tm0 = GPROF_T();
     for (int tile = tb0, it = 0; tile < tb1; ++tile, ++it) {
       const int kv = bhkv_of(tile);
       if (kv != cur) {
@@ -424,9 +424,9 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
         ++n_img;
       }
       const int qb = it % C::NQB, tb = it & 1;
-      const long long tq0 = GPROF_T();
+      [[maybe_unused]] const long long tq0 = GPROF_T();
       ptx::mbar_wait(&q_full[qb], (it / C::NQB) & 1u);
-      const long long tq1 = GPROF_T();
+      [[maybe_unused]] const long long tq1 = GPROF_T();
       ptx::mbar_wait(&t_empty[tb], ((it >> 1) & 1u) ^ 1u);
       if (lp) {
         GPROF_ADD(0, tq1 - tq0);
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(320, 1) gram_apply_kernel(const __grid_constan
         const int chunk = hf * (HD / 8) + j, kb = chunk >> 3, cj = chunk & 7;
         qv[j] = *reinterpret_cast<const uint4*>(qrow + kb * BLK + ((cj ^ (r & 7)) << 4));
       }
-      const long long te0 = GPROF_T();
+      [[maybe_unused]] const long long te0 = GPROF_T();
       ptx::mbar_wait(&t_full[tb], (it >> 1) & 1u);
       if (warp == 2 && lane == 0) GPROF_ADD(5, GPROF_T() - te0);
       ptx::tc_fence_after();

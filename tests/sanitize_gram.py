@@ -14,6 +14,15 @@ for dt in (torch.bfloat16, torch.float16):
         m = torch.randint(0, 6, (2, 700), generator=g, device="cuda").float()
         fs.gram_fwd(q, k[:, :, :2], v[:, :, :2], key_scale=m, check=False)
         fs.gram_fwd(q, k, v, out_dtype=torch.float32, check=False)
+if os.environ.get("SANITIZE_GRAM_BIG") == "1":
+    # ~7 query tiles per CTA: the apply kernel's Q ring and accumulator buffers wrap
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v = (torch.randn((4, 4096, 8, 128), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+    fs.gram_fwd(q, k, v, check=False)
+    if os.environ.get("SANITIZE_GRAM_ONLY") == "1":
+        torch.cuda.synchronize()
+        print("sanitize_gram ok")
+        sys.exit(0)
 torch.cuda.synchronize()
 print("sanitize_gram ok")
 # the float64 mode kernel (fs_exact_fwd) through the drop-in API
